@@ -1,0 +1,362 @@
+/*
+ * oracle.cpp — the CPU ORACLE for the Gerbil counting phase.
+ *
+ *   *** TEST INFRASTRUCTURE. Only tests/, __graft_entry__.smoke() and
+ *   *** bench.py's cpu_baseline / --impl reference leg may load this library.
+ *   *** The product path (paper_1607_06618_b200/) never imports, links or
+ *   *** executes anything under oracle/.
+ *
+ * A plain, slow, obviously correct implementation of what the path computes,
+ * written from PAPER.md and sharing no code with the CUDA path (its own
+ * parser, its own reverse complement, its own ordering, std::string keys in a
+ * std::map). Every function cites the passage it follows.
+ *
+ *  - oracle_count: the k-mer histogram (Abstract: "build a
+ *    histogram of all substrings of length k"), canonical = lexicographically
+ *    smaller of x and rc(x) (§2.4.2), ignoring k-mers with
+ *    an undetermined base (§2.4.1), output iff
+ *    count >= min_count (`-l`). Pinned by tests/test_oracle.py
+ *    (brute force, `sort | uniq -c`, de Bruijn closed forms, planted
+ *    multiplicities, Σ-count identity, rc invariance).
+ *  - oracle_minimizer / oracle_supermers: minimizer = smallest m-substring
+ *    under a total order (§2.1); super-mers = maximal substrings
+ *    whose k-mers share one minimizer (Fig. 1);
+ *    orderings LEX (A<C<G<T, Fig. 1) and KMC2 (A<C<G<T with the AAA/ACA
+ *    prefixes demoted; reading Q9 in DESIGN.md). Pinned by the
+ *    Fig. 1 example and SPEC.md:81-82 minimizer examples.
+ *  - oracle_count_sampled: the same histogram restricted to canonical k-mers
+ *    whose FNV-1a-64 hash of the ASCII string is ≡ 0 (mod `mod`) — the
+ *    full-scale parity check of SURVEY.md §8(c) "Scale strategy". Pinned by
+ *    equality with oracle_count filtered by the same predicate.
+ *
+ * Input parsing (reading Q3/Q4 in DESIGN.md): FASTA ('>' header, multi-line
+ * sequence concatenated), FASTQ ('@' header, sequence, '+' [header],
+ * quality of equal length), or raw (one read per line) when the first
+ * non-empty byte is neither '>' nor '@'. CR bytes are dropped, empty lines
+ * skipped; lowercase is folded; every other byte outside ACGT breaks the read.
+ */
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+struct Result {
+  std::vector<std::string> kmers;
+  std::vector<uint64_t> counts;
+  uint64_t windows = 0;   /* valid windows seen (Σ counts before threshold) */
+  uint64_t distinct = 0;  /* distinct canonical k-mers before threshold */
+  std::string error;
+};
+
+/* ---- parsing (App. B; Q3/Q4) ------------------- */
+
+/* Splits text into lines without CR; returns false + message on malformed. */
+static void split_lines(const char* text, size_t len, std::vector<std::string>& lines) {
+  size_t i = 0;
+  while (i < len) {
+    size_t j = i;
+    while (j < len && text[j] != '\n') ++j;
+    std::string line(text + i, j - i);
+    line.erase(std::remove(line.begin(), line.end(), '\r'), line.end());
+    lines.push_back(line);
+    i = j + 1;
+  }
+}
+
+static bool parse_reads(const char* text, size_t len, std::vector<std::string>& reads,
+                        std::string& err) {
+  std::vector<std::string> lines;
+  split_lines(text, len, lines);
+  size_t first = 0;
+  while (first < lines.size() && lines[first].empty()) ++first;
+  if (first == lines.size()) return true; /* empty input: no reads */
+  char kind = lines[first][0];
+  if (kind == '>') {
+    std::string cur;
+    bool have = false;
+    for (size_t i = first; i < lines.size(); ++i) {
+      const std::string& l = lines[i];
+      if (l.empty()) continue;
+      if (l[0] == '>') {
+        if (have) reads.push_back(cur);
+        cur.clear();
+        have = true;
+      } else {
+        cur += l;
+      }
+    }
+    if (have) reads.push_back(cur);
+    return true;
+  }
+  if (kind == '@') {
+    size_t i = first;
+    while (i < lines.size()) {
+      if (lines[i].empty()) { ++i; continue; }
+      if (lines[i][0] != '@') {
+        err = "FASTQ: expected '@' at line " + std::to_string(i + 1);
+        return false;
+      }
+      if (i + 3 >= lines.size()) {
+        err = "FASTQ: truncated record at line " + std::to_string(i + 1);
+        return false;
+      }
+      const std::string& seq = lines[i + 1];
+      const std::string& plus = lines[i + 2];
+      const std::string& qual = lines[i + 3];
+      if (plus.empty() || plus[0] != '+') {
+        err = "FASTQ: expected '+' at line " + std::to_string(i + 3);
+        return false;
+      }
+      if (qual.size() != seq.size()) {
+        err = "FASTQ: quality length mismatch at line " + std::to_string(i + 4);
+        return false;
+      }
+      reads.push_back(seq);
+      i += 4;
+    }
+    return true;
+  }
+  for (size_t i = first; i < lines.size(); ++i)
+    if (!lines[i].empty()) reads.push_back(lines[i]);
+  return true;
+}
+
+/* Case-fold, then break at every byte outside {A,C,G,T}. */
+static void fragments_of(const std::string& read, std::vector<std::string>& out) {
+  std::string cur;
+  for (char ch : read) {
+    char u = (ch >= 'a' && ch <= 'z') ? (char)(ch - 'a' + 'A') : ch;
+    if (u == 'A' || u == 'C' || u == 'G' || u == 'T') {
+      cur.push_back(u);
+    } else {
+      if (!cur.empty()) out.push_back(cur);
+      cur.clear();
+    }
+  }
+  if (!cur.empty()) out.push_back(cur);
+}
+
+/* ---- k-mer definitions (§2.4.2) ----------------------- */
+
+static char complement(char c) {
+  switch (c) {
+    case 'A': return 'T';
+    case 'T': return 'A';
+    case 'C': return 'G';
+    case 'G': return 'C';
+  }
+  return c;
+}
+
+/* "reversing x and replacing A⇔T and C⇔G" */
+static std::string reverse_complement(const std::string& x) {
+  std::string r(x.rbegin(), x.rend());
+  for (char& c : r) c = complement(c);
+  return r;
+}
+
+/* "the lexicographically smaller k-mer as canonical representation";
+ * ASCII 'A'<'C'<'G'<'T' is the paper's A<C<G<T order (reading Q1). */
+static std::string canonical(const std::string& x) {
+  std::string r = reverse_complement(x);
+  return r < x ? r : x;
+}
+
+static uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (char c : s) {
+    h ^= (unsigned char)c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+/* Count every window of every fragment into the map. */
+static void count_reads(const std::vector<std::string>& reads, size_t r0, size_t r1,
+                        uint32_t k, int canon, uint64_t mod,
+                        std::map<std::string, uint64_t>& hist, uint64_t& windows) {
+  std::vector<std::string> frags;
+  for (size_t r = r0; r < r1; ++r) {
+    frags.clear();
+    fragments_of(reads[r], frags);
+    for (const std::string& f : frags) {
+      if (f.size() < k) continue;
+      for (size_t i = 0; i + k <= f.size(); ++i) {
+        std::string w = f.substr(i, k);
+        std::string c = canon ? canonical(w) : w;
+        ++windows;
+        if (mod > 1 && fnv1a(c) % mod != 0) continue;
+        ++hist[c];
+      }
+    }
+  }
+}
+
+static Result* finish(std::map<std::string, uint64_t>& hist, uint64_t windows,
+                      uint32_t min_count) {
+  Result* res = new Result();
+  res->windows = windows;
+  res->distinct = hist.size();
+  for (auto& kv : hist)
+    if (kv.second >= min_count) {
+      res->kmers.push_back(kv.first);
+      res->counts.push_back(kv.second);
+    }
+  return res;
+}
+
+/* ---- minimizers and super-mers (§2.1; §3.1) ------------- */
+
+/* Ordering "less than" on two m-mers. LEX: A<C<G<T. KMC2: the same, except
+ * that m-mers starting with AAA or ACA come after all others,
+ * lexicographic inside each group (reading Q9). */
+static bool order_less(const std::string& a, const std::string& b, int ordering) {
+  if (ordering == 0 && a.size() >= 3) {
+    bool da = a.compare(0, 3, "AAA") == 0 || a.compare(0, 3, "ACA") == 0;
+    bool db = b.compare(0, 3, "AAA") == 0 || b.compare(0, 3, "ACA") == 0;
+    if (da != db) return db; /* non-demoted < demoted */
+  }
+  return a < b;
+}
+
+/* "a minimizer of a k-mer is defined as its lexicographically smallest
+ * substring of a fixed length m < k with respect to some total ordering"
+ * (PAPER.md:51). symmetric = minimum over the m-mers of x and of rc(x)
+ * (reading Q7: required for canonical bins). */
+static std::string minimizer_of(const std::string& x, uint32_t m, int ordering,
+                                int symmetric) {
+  std::string best;
+  bool have = false;
+  std::string rx = reverse_complement(x);
+  for (size_t j = 0; j + m <= x.size(); ++j) {
+    std::string f = x.substr(j, m);
+    if (!have || order_less(f, best, ordering)) { best = f; have = true; }
+    if (symmetric) {
+      std::string g = rx.substr(j, m);
+      if (order_less(g, best, ordering)) best = g;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" {
+
+typedef struct oracle_result oracle_result;
+
+/* Full histogram of a FASTA/FASTQ/raw document. Returns NULL on parse error
+ * (message copied into err). canon=0 counts k-mers as they occur (-d,
+ * PAPER.md:483). */
+oracle_result* oracle_count(const char* text, uint64_t len, uint32_t k,
+                            uint32_t min_count, int canon, char* err, uint64_t err_len) {
+  std::vector<std::string> reads;
+  std::string e;
+  if (!parse_reads(text, len, reads, e)) {
+    if (err && err_len) { strncpy(err, e.c_str(), err_len - 1); err[err_len - 1] = 0; }
+    return nullptr;
+  }
+  std::map<std::string, uint64_t> hist;
+  uint64_t windows = 0;
+  count_reads(reads, 0, reads.size(), k, canon, 1, hist, windows);
+  return (oracle_result*)finish(hist, windows, min_count);
+}
+
+/* Hash-sampled histogram on `threads` host threads: only canonical k-mers
+ * with fnv1a(string) % mod == 0 are kept; windows counts all valid windows. */
+oracle_result* oracle_count_sampled(const char* text, uint64_t len, uint32_t k,
+                                    uint32_t min_count, uint64_t mod, int threads,
+                                    char* err, uint64_t err_len) {
+  std::vector<std::string> reads;
+  std::string e;
+  if (!parse_reads(text, len, reads, e)) {
+    if (err && err_len) { strncpy(err, e.c_str(), err_len - 1); err[err_len - 1] = 0; }
+    return nullptr;
+  }
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  std::vector<std::map<std::string, uint64_t>> parts(threads);
+  std::vector<uint64_t> wins(threads, 0);
+  std::vector<std::thread> ts;
+  size_t per = (reads.size() + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    size_t a = std::min(reads.size(), t * per), b = std::min(reads.size(), a + per);
+    ts.emplace_back([&, t, a, b] { count_reads(reads, a, b, k, 1, mod, parts[t], wins[t]); });
+  }
+  for (auto& t : ts) t.join();
+  std::map<std::string, uint64_t> hist;
+  uint64_t windows = 0;
+  for (int t = 0; t < threads; ++t) {
+    windows += wins[t];
+    for (auto& kv : parts[t]) hist[kv.first] += kv.second;
+  }
+  return (oracle_result*)finish(hist, windows, min_count);
+}
+
+uint64_t oracle_result_n(const oracle_result* r) { return ((const Result*)r)->kmers.size(); }
+uint64_t oracle_result_windows(const oracle_result* r) { return ((const Result*)r)->windows; }
+uint64_t oracle_result_distinct(const oracle_result* r) { return ((const Result*)r)->distinct; }
+
+/* kmers: n*k bytes (no separators), counts: n entries, in A<C<G<T order. */
+void oracle_result_get(const oracle_result* r, char* kmers, uint64_t* counts) {
+  const Result* res = (const Result*)r;
+  for (size_t i = 0; i < res->kmers.size(); ++i) {
+    if (kmers) memcpy(kmers + i * res->kmers[i].size(), res->kmers[i].data(), res->kmers[i].size());
+    if (counts) counts[i] = res->counts[i];
+  }
+}
+
+void oracle_result_free(oracle_result* r) { delete (Result*)r; }
+
+/* fnv1a(kmer) % mod == 0 — the sampling predicate, exposed for harnesses. */
+int oracle_sample_keep(const char* kmer, uint32_t k, uint64_t mod) {
+  return fnv1a(std::string(kmer, k)) % mod == 0;
+}
+
+void oracle_reverse_complement(const char* x, uint32_t n, char* out) {
+  std::string r = reverse_complement(std::string(x, n));
+  memcpy(out, r.data(), n);
+}
+
+void oracle_canonical(const char* x, uint32_t n, char* out) {
+  std::string c = canonical(std::string(x, n));
+  memcpy(out, c.data(), n);
+}
+
+/* Minimizer m-mer of one k-mer (ordering 0 = KMC2, 1 = LEX). */
+void oracle_minimizer(const char* kmer, uint32_t k, uint32_t m, int ordering,
+                      int symmetric, char* out) {
+  std::string mm = minimizer_of(std::string(kmer, k), m, ordering, symmetric);
+  memcpy(out, mm.data(), m);
+}
+
+/* Super-mers of one ACGT-only fragment: maximal runs of consecutive k-mers
+ * whose minimizers are equal (Fig. 1). Writes the super-mers
+ * separated by '\n' into out (if large enough); returns the bytes needed. */
+uint64_t oracle_supermers(const char* seq, uint32_t len, uint32_t k, uint32_t m,
+                          int ordering, int symmetric, char* out, uint64_t cap) {
+  std::string s(seq, len), text;
+  if (len >= k) {
+    size_t nwin = len - k + 1;
+    std::vector<std::string> mu(nwin);
+    for (size_t p = 0; p < nwin; ++p) mu[p] = minimizer_of(s.substr(p, k), m, ordering, symmetric);
+    size_t p0 = 0;
+    for (size_t p = 1; p <= nwin; ++p) {
+      if (p == nwin || mu[p] != mu[p0]) {
+        /* windows p0..p-1 share one minimizer: bases [p0, p-1+k) */
+        text += s.substr(p0, (p - 1 - p0) + k);
+        text += '\n';
+        p0 = p;
+      }
+    }
+  }
+  if (out && cap >= text.size()) memcpy(out, text.data(), text.size());
+  return text.size();
+}
+
+} /* extern "C" */

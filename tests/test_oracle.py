@@ -1,0 +1,313 @@
+"""Pins of the CPU oracle (oracle/oracle.cpp) against what the paper and the
+mathematics fix — never against the oracle itself.
+
+Each test names the passage or closed form it checks. A plausible mistake in
+the oracle (dropped complement, reverse-only rc, wrong canonical side, k-mers
+spanning an N or two reads, off-by-one window count, wrong threshold sense,
+broken FASTQ/FASTA parsing) fails at least one of them.
+"""
+import os
+import random
+import subprocess
+
+import pytest
+
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    rows = []
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            rows.append(line)
+    return rows
+
+
+# ---- §2.4.2 reverse complement / canonical ---------------------------------
+def test_rc_paper_example():
+    # "the k-mer ACCG corresponds to CGGT"
+    assert oracle.reverse_complement(b"ACCG") == b"CGGT"
+    assert oracle.reverse_complement(b"CGGT") == b"ACCG"
+
+
+def test_rc_involution_and_palindrome():
+    rnd = random.Random(7)
+    for _ in range(200):
+        x = bytes(rnd.choice(b"ACGT") for _ in range(rnd.randint(1, 90)))
+        assert oracle.reverse_complement(oracle.reverse_complement(x)) == x
+    assert oracle.reverse_complement(b"AT") == b"AT"  # SPEC.md:64 (palindrome)
+
+
+def test_canonical_examples():
+    # canonicalize(ACCG)=ACCG, canonicalize(CGGT)=ACCG, idempotent
+    assert oracle.canonical(b"ACCG") == b"ACCG"
+    assert oracle.canonical(b"CGGT") == b"ACCG"
+    rnd = random.Random(3)
+    for _ in range(100):
+        x = bytes(rnd.choice(b"ACGT") for _ in range(31))
+        c = oracle.canonical(x)
+        assert oracle.canonical(c) == c
+        assert c in (x, oracle.reverse_complement(x)) and c <= x
+
+
+# ---- §2.1 minimizers / super-mers (Fig. 1) -----------------------------------
+def test_fig1_supermers_forward_lex():
+    rows = _golden("fig1_supermers.txt")
+    seq = rows[0].split()[1].encode()
+    k, m = int(rows[1].split()[1]), int(rows[2].split()[1])
+    expect = [r.encode() for r in rows[3:]]
+    assert oracle.supermers(seq, k, m, oracle.LEX, symmetric=False) == expect
+
+
+def test_fig1_supermers_strand_symmetric_same_boundaries():
+    # SURVEY.md §8(c) pins: the strand-symmetric minimizers give the same five super-mers
+    rows = _golden("fig1_supermers.txt")
+    expect = [r.encode() for r in rows[3:]]
+    assert oracle.supermers(b"CAAGAACAGTG", 4, 3, oracle.LEX, symmetric=True) == expect
+
+
+def test_minimizer_examples():
+    # SPEC.md:81-82 (Fig. 1 bold parts): CAAG → AAG, ACAG → ACA (lexicographic, forward)
+    assert oracle.minimizer(b"CAAG", 3, oracle.LEX, symmetric=False) == b"AAG"
+    assert oracle.minimizer(b"ACAG", 3, oracle.LEX, symmetric=False) == b"ACA"
+    # KMC2: m-mers starting with AAA / ACA are demoted behind all others
+    assert oracle.minimizer(b"AAAC", 3, oracle.KMC2, symmetric=False) == b"AAC"
+    assert oracle.minimizer(b"ACAT", 3, oracle.KMC2, symmetric=False) == b"CAT"
+    assert oracle.minimizer(b"AAAA", 3, oracle.KMC2, symmetric=False) == b"AAA"  # only choice
+    # both demoted prefixes lose to any other m-mer: LEX picks AAA, KMC2 picks CAA
+    assert oracle.minimizer(b"ACAAA", 3, oracle.LEX, symmetric=False) == b"AAA"
+    assert oracle.minimizer(b"ACAAA", 3, oracle.KMC2, symmetric=False) == b"CAA"
+
+
+def test_minimizer_strand_symmetry():
+    # minimizer(x) = minimizer(rc(x)) when strand-symmetric
+    rnd = random.Random(11)
+    for _ in range(300):
+        x = bytes(rnd.choice(b"ACGT") for _ in range(rnd.randint(8, 40)))
+        m = rnd.randint(2, 7)
+        for ordering in (oracle.KMC2, oracle.LEX):
+            assert oracle.minimizer(x, m, ordering) == oracle.minimizer(oracle.reverse_complement(x), m, ordering)
+
+
+def test_supermer_window_multiset_and_shared_minimizer():
+    # PAPER.md:51 (definition) and SPEC.md:87/97: windows of the super-mers = windows of the
+    # fragment; every window of a super-mer has the same minimizer; 1 <= #super-mers <= L-k+1
+    rnd = random.Random(5)
+    for _ in range(100):
+        L = rnd.randint(10, 80)
+        k = rnd.randint(4, min(L, 20))
+        m = rnd.randint(2, k - 1)
+        seq = bytes(rnd.choice(b"ACGT") for _ in range(L))
+        sms = oracle.supermers(seq, k, m, oracle.KMC2, symmetric=True)
+        wins = sorted(seq[i:i + k] for i in range(L - k + 1))
+        got = sorted(s[i:i + k] for s in sms for i in range(len(s) - k + 1))
+        assert wins == got
+        assert 1 <= len(sms) <= L - k + 1
+        for s in sms:
+            mins = {oracle.minimizer(s[i:i + k], m, oracle.KMC2) for i in range(len(s) - k + 1)}
+            assert len(mins) == 1
+
+
+# ---- the histogram ---------------------------------------------------------
+def test_fig1_counts_golden():
+    expect = {}
+    for r in _golden("canonical_fig1_counts.txt"):
+        a, b = r.split()
+        expect[a.encode()] = int(b)
+    res = oracle.count(b">fig1\nCAAGAACAGTG\n", 4)
+    assert res.as_dict() == expect
+    assert res.windows == 8
+    # min_count=2 → nothing (PAPER.md:467 threshold, reading Q5: output iff count >= l)
+    assert oracle.count(b">fig1\nCAAGAACAGTG\n", 4, min_count=2).kmers == []
+
+
+def test_undetermined_bases():
+    # PAPER.md:122 "we ignore all k-mers that contain an undetermined base"
+    assert oracle.count(b">r\nACGTNACGT\n", 4).as_dict() == {b"ACGT": 2}
+    assert oracle.count(b">r\nACGNT\n", 4).as_dict() == {}
+    # IUPAC letters and '.' are undetermined too (reading Q3); lowercase counts
+    assert oracle.count(b">r\nacgtRACGT.acgt\n", 4).as_dict() == {b"ACGT": 3}
+
+
+def test_threshold_sense():
+    text = b">a\nAAAAAA\n"  # A^6, k=4 → AAAA x3
+    assert oracle.count(text, 4, min_count=3).as_dict() == {b"AAAA": 3}
+    assert oracle.count(text, 4, min_count=4).as_dict() == {}
+
+
+def test_all_a_closed_form():
+    # closed form: a read A^L has the single canonical k-mer A^k with count L-k+1
+    for L, k in ((50, 28), (300, 200), (33, 32)):
+        assert oracle.count(b">a\n" + b"A" * L + b"\n", k).as_dict() == {b"A" * k: L - k + 1}
+        assert oracle.count(b">t\n" + b"T" * L + b"\n", k).as_dict() == {b"A" * k: L - k + 1}
+
+
+def _de_bruijn(n):
+    """Standard recursive (Lyndon-word) construction of B(4, n), linearised."""
+    a = [0] * 4 * n
+    seq = []
+
+    def db(t, p):
+        if t > n:
+            if n % p == 0:
+                seq.extend(a[1:p + 1])
+        else:
+            a[t] = a[t - p]
+            db(t + 1, p)
+            for j in range(a[t - p] + 1, 4):
+                a[t] = j
+                db(t + 1, t)
+
+    db(1, 1)
+    s = bytes(b"ACGT"[x] for x in seq)
+    return s + s[: n - 1]
+
+
+@pytest.mark.parametrize("k", [8, 9])
+def test_de_bruijn_closed_form(k):
+    # Linear de Bruijn B(4,k): every k-mer occurs exactly once as a window (4^k windows).
+    # Canonically, x and rc(x) merge → count 2, except rc-palindromes (only for even k:
+    # 4^(k/2) of them) which keep count 1.
+    s = _de_bruijn(k)
+    assert len(s) == 4**k + k - 1
+    res = oracle.count(b">db\n" + s + b"\n", k)
+    hist = {}
+    for c in res.counts:
+        hist[c] = hist.get(c, 0) + 1
+    if k % 2 == 0:
+        pal = 4 ** (k // 2)
+        assert hist == {2: (4**k - pal) // 2, 1: pal}
+    else:
+        assert hist == {2: 4**k // 2}
+    assert res.windows == 4**k
+
+
+def test_sum_counts_equals_valid_windows():
+    # Σ counts (min_count=1) = Σ over N-free fragments of max(0, |F|-k+1)
+    rnd = random.Random(2)
+    reads = []
+    for _ in range(60):
+        reads.append(bytes(rnd.choice(b"ACGTACGTACGTN") for _ in range(rnd.randint(1, 120))))
+    text = b"".join(b">r\n" + r + b"\n" for r in reads)
+    for k in (8, 13, 31, 32, 33):
+        res = oracle.count(text, k)
+        expect = 0
+        for r in reads:
+            for frag in r.split(b"N"):
+                expect += max(0, len(frag) - k + 1)
+        assert sum(res.counts) == expect == res.windows
+
+
+def test_grch38_identity():
+    # PAPER.md:284 (Table 1): GRCh38 has 97,300,000,000 28-mers for 10^8 reads of length 1000,
+    # i.e. exactly 1000-28+1 = 973 windows per N-free read. Same identity at small scale.
+    rnd = random.Random(9)
+    reads = [bytes(rnd.choice(b"ACGT") for _ in range(1000)) for _ in range(5)]
+    res = oracle.count(b"".join(b">r\n" + r + b"\n" for r in reads), 28)
+    assert res.windows == 5 * 973 and 97_300_000_000 == 10**8 * 973
+
+
+def test_rc_input_doubles_counts():
+    # invariance: counting R ∪ rc(R) gives exactly twice the counts of R (canonical counting)
+    rnd = random.Random(4)
+    reads = [bytes(rnd.choice(b"ACGT") for _ in range(rnd.randint(30, 90))) for _ in range(40)]
+    t1 = b"".join(b">r\n" + r + b"\n" for r in reads)
+    t2 = t1 + b"".join(b">q\n" + oracle.reverse_complement(r) + b"\n" for r in reads)
+    a, b = oracle.count(t1, 21).as_dict(), oracle.count(t2, 21).as_dict()
+    assert b == {x: 2 * c for x, c in a.items()}
+
+
+def test_planted_multiplicities():
+    # Reads cut from disjoint stretches of a random 200 kbp sequence (all 28-mers distinct
+    # w.h.p.), read i repeated c_i times (random strand) → the count histogram is known by
+    # construction: each read contributes L_i-27 distinct k-mers with count c_i.
+    rnd = random.Random(12)
+    genome = bytes(rnd.choice(b"ACGT") for _ in range(200_000))
+    text = []
+    expect_hist = {}
+    pos = 0
+    for i in range(300):
+        L = rnd.randint(28, 150)
+        r = genome[pos:pos + L]
+        pos += L + 30
+        c = rnd.randint(1, 5)
+        for _ in range(c):
+            text.append(b">p\n" + (r if rnd.random() < 0.5 else oracle.reverse_complement(r)) + b"\n")
+        expect_hist[c] = expect_hist.get(c, 0) + (L - 27)
+    res = oracle.count(b"".join(text), 28)
+    hist = {}
+    for c in res.counts:
+        hist[c] = hist.get(c, 0) + 1
+    assert hist == expect_hist
+
+
+def test_sort_uniq_textbook(tmp_path):
+    # textbook routine: coreutils `sort | uniq -c` over the canonical windows printed one per
+    # line must equal the oracle's histogram (canonical side chosen by the oracle's rc
+    # per window is pinned above; here the counting/grouping is checked independently).
+    rnd = random.Random(21)
+    reads = [bytes(rnd.choice(b"ACGT") for _ in range(rnd.randint(20, 60))) for _ in range(50)]
+    k = 12
+    lines = []
+    for r in reads:
+        for i in range(len(r) - k + 1):
+            lines.append(oracle.canonical(r[i:i + k]))
+    p = tmp_path / "w.txt"
+    p.write_bytes(b"\n".join(lines) + b"\n")
+    out = subprocess.run(f"LC_ALL=C sort {p} | uniq -c", shell=True, capture_output=True, check=True).stdout
+    textbook = {}
+    for line in out.decode().splitlines():
+        c, w = line.split()
+        textbook[w.encode()] = int(c)
+    res = oracle.count(b"".join(b">r\n" + r + b"\n" for r in reads), k)
+    assert res.as_dict() == textbook
+    assert res.kmers == sorted(textbook)  # map order is A<C<G<T (ASCII) order
+
+
+# ---- parsing (reading Q3/Q4) ---------------------------------------------------------
+def test_fasta_fastq_raw_agree_and_multiline():
+    rnd = random.Random(8)
+    reads = [bytes(rnd.choice(b"ACGTN") for _ in range(rnd.randint(40, 120))) for _ in range(30)]
+    fa = b"".join(b">r%d\n" % i + r + b"\n" for i, r in enumerate(reads))
+    fa_ml = b"".join(b">r%d\n" % i + b"\n".join(r[j:j + 17] for j in range(0, len(r), 17)) + b"\n"
+                     for i, r in enumerate(reads))
+    fq = b"".join(b"@r%d\n" % i + r + b"\n+\n" + b"I" * len(r) + b"\n" for i, r in enumerate(reads))
+    fq_h = b"".join(b"@r%d\n" % i + r + b"\n+r%d\n" % i + b"@" * len(r) + b"\n" for i, r in enumerate(reads))
+    raw = b"".join(r + b"\n" for r in reads)
+    crlf = fa.replace(b"\n", b"\r\n")
+    lower = fa.lower().replace(b">r", b">R")
+    ref = oracle.count(fa, 25).as_dict()
+    for t in (fa_ml, fq, fq_h, raw, crlf, lower):
+        assert oracle.count(t, 25).as_dict() == ref
+    # a read never continues into the next record (k-mers never span reads)
+    two = oracle.count(b">a\nACGTA\n>b\nCGTAC\n", 6)
+    assert two.windows == 0
+
+
+def test_malformed_fastq_is_an_error():
+    with pytest.raises(ValueError):
+        oracle.count(b"@r\nACGT\n-\nIIII\n", 4)
+    with pytest.raises(ValueError):
+        oracle.count(b"@r\nACGT\n+\nIII\n", 4)
+    with pytest.raises(ValueError):
+        oracle.count(b"@r\nACGT\n+\n", 4)
+
+
+def test_empty_input():
+    # empty input → empty output
+    r = oracle.count(b"", 28)
+    assert r.kmers == [] and r.windows == 0
+
+
+def test_sampled_equals_filtered_full():
+    rnd = random.Random(6)
+    reads = [bytes(rnd.choice(b"ACGT") for _ in range(200)) for _ in range(200)]
+    text = b"".join(b">r\n" + r + b"\n" for r in reads)
+    full = oracle.count(text, 31)
+    samp = oracle.count_sampled(text, 31, mod=16, threads=3)
+    expect = {x: c for x, c in full.as_dict().items() if oracle.sample_keep(x, 16)}
+    assert samp.as_dict() == expect and len(expect) > 0
+    assert samp.windows == full.windows
