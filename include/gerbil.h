@@ -1,0 +1,206 @@
+/*
+ * gerbil.h — C ABI of the B200-native Gerbil counting phase.
+ *
+ * What the library computes (Abstract): the histogram of all
+ * length-k substrings of a set of reads, counting each k-mer under its
+ * canonical representation min(x, rc(x)) (§2.4.2), ignoring
+ * every k-mer that contains an undetermined base (§2.4.1),
+ * and reporting the (k-mer, count) pairs whose count reaches a threshold
+ * (App. A `-l`).
+ *
+ * How (§2): reads are cut into minimizer super-mers
+ * (§2.1) and every super-mer is assigned to a bin, so that all
+ * occurrences of a k-mer fall in one bin; bins are shuffled to
+ * their owner GPU (NCCL all-to-all, world > 1) and counted independently in a
+ * bucketised open-addressing hash table (PAPER.md:63-84, Alg. 1; :171-178,
+ * §3.3.1) with an exact emergency path for k-mers that exhaust θ probes
+ * (§3.4.3). Steps (a)-(e) of SURVEY.md §8(a).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - 2-bit base code: A=0, C=1, G=2, T=3 (App. C).
+ *  - Packed base stream: base i of a batch lives in 64-bit word i/32, bits
+ *    [63-2(i%32) : 62-2(i%32)] (first base in the most significant bits,
+ *    PAPER.md:517-518).
+ *  - N-mask: bit (63 - i%64) of word i/64 is 1 iff base i is undetermined
+ *    (any byte outside {A,C,G,T,a,c,g,t} in the text).
+ *  - read_start[0..n_reads]: base offset of read r is read_start[r]; its
+ *    length is read_start[r+1]-read_start[r]; read_start[0] == 0. k-mers never
+ *    span two reads.
+ *  - Result key layout: W = ceil(k/32) u64 words per k-mer; word 0 holds bases
+ *    0..31 with base 0 in bits 63:62; the last word is left-aligned and
+ *    zero-padded. A big-endian dump of the words truncated to ceil(k/4) bytes
+ *    is exactly the appendix k-mer byte encoding, and the
+ *    numeric order of the word arrays equals A<C<G<T string order.
+ *
+ * Ownership: the caller owns every input buffer; inputs are read-only during
+ * the call and never retained. The library owns its device memory, streams
+ * and results until the next gerbil_count* call or gerbil_finalize.
+ * gerbil_fetch copies into caller-allocated buffers. Calls on one context
+ * must be serialised by the caller. No C++ exception crosses this ABI.
+ *
+ * Errors: every call returns a gerbil_status. GERBIL_E_USAGE for invalid
+ * arguments (nothing is changed); GERBIL_E_IO for unreadable/malformed input
+ * (message with file and line via gerbil_last_error); GERBIL_E_INTERNAL when
+ * the Σcount == #valid-windows invariant fails; GERBIL_E_CUDA /
+ * GERBIL_E_NCCL poison the context (only gerbil_finalize is then valid);
+ * GERBIL_E_STATE for gerbil_fetch before a successful count.
+ */
+#ifndef GERBIL_H
+#define GERBIL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GERBIL_ABI_VERSION 1
+
+typedef struct gerbil_ctx gerbil_ctx;
+
+typedef enum {
+  GERBIL_OK = 0,
+  GERBIL_E_USAGE = 1,
+  GERBIL_E_IO = 2,
+  GERBIL_E_INTERNAL = 3,
+  GERBIL_E_NOMEM = 4,
+  GERBIL_E_CUDA = 5,
+  GERBIL_E_NCCL = 6,
+  GERBIL_E_STATE = 7
+} gerbil_status;
+
+/* Minimizer orderings (§3.1). KMC2 is Gerbil's choice
+ * (PAPER.md:157); LEX (A<C<G<T) is the ordering of Fig. 1. */
+typedef enum { GERBIL_ORDER_KMC2 = 0, GERBIL_ORDER_LEX = 1 } gerbil_ordering;
+
+typedef struct {
+  uint32_t struct_size;    /* sizeof(gerbil_config); ABI versioning */
+  int32_t device;          /* CUDA device ordinal of this rank; -1 = current */
+  int32_t rank, world;     /* multi-process mode, one GPU per rank; 0/1 = single */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId when world > 1, else NULL */
+  int32_t comm_backend;    /* 0 = NCCL (one process per GPU); 1 = loopback: `world`
+                              contexts in ONE process on one GPU, driven from `world`
+                              host threads, exchanging by device copies (test seam;
+                              nccl_unique_id = any 128-byte group key) */
+  uint32_t n_bins;         /* B (temporary-file analogue, PAPER.md:459 `-f`); 0 = auto (>= 512) */
+  int32_t ordering;        /* gerbil_ordering; 0 = KMC2 */
+  uint64_t device_mem_cap; /* bytes of device memory the library may allocate; 0 = auto (`-e`) */
+  int32_t host_threads;    /* host reader threads; 0 = all cores (`-t`) */
+  uint32_t max_probes;     /* θ in buckets; 0 = 32 */
+  double distinct_ratio;   /* initial ρ̂ = distinct/total estimate; 0 = 0.5 */
+  double target_load;      /* α: table load factor target; 0 = 0.7 */
+  uint64_t wave_table_bytes; /* per-wave table budget (kept L2-resident); 0 = 64 MiB */
+  void* stream;            /* cudaStream_t to launch on; NULL = library-owned stream */
+  int32_t timing;          /* 1 = record per-kernel CUDA-event times into gerbil_stats */
+} gerbil_config;
+
+/* Exactly one source must be set. */
+typedef struct {
+  const char* const* paths; uint32_t n_paths; /* FASTA/FASTQ files (App. B) */
+  const char* text; uint64_t text_len;        /* one in-memory FASTA or FASTQ document */
+} gerbil_reads;
+
+typedef struct {
+  /* sizes (whole job = all ranks, except where noted "local") */
+  uint64_t input_bases;      /* local: all input bases incl. undetermined ones */
+  uint64_t input_reads;      /* local */
+  uint64_t valid_windows;    /* local: n_k, k-mer windows with no undetermined base */
+  uint64_t supermers;        /* local: super-mers produced by step (b) */
+  uint64_t owned_windows;    /* windows counted on this rank after the shuffle */
+  uint64_t distinct;         /* distinct canonical k-mers counted on this rank */
+  uint64_t kept;             /* of which count >= min_count (returned by fetch) */
+  uint64_t count_sum;        /* Σ counts over all table slots + overflow (== owned_windows) */
+  uint64_t overflow_kmers;   /* k-mer occurrences that exhausted θ probes (emergency path) */
+  uint64_t probe_first;      /* inserts resolved in the first bucket */
+  uint64_t probe_more;       /* inserts that needed more than one bucket */
+  uint64_t probe_max;        /* most buckets probed by one insert */
+  uint32_t overflow_passes;  /* extra counting passes spent on the emergency path */
+  uint32_t waves;            /* table waves run by step (d) */
+  uint32_t n_bins;
+  uint32_t W;                /* key words per k-mer */
+  uint64_t max_bin_windows;  /* largest bin (global), for skew reporting */
+  uint64_t bytes_sent, bytes_recv; /* step (c) NVLink traffic of this rank */
+  double ratio_used;         /* ρ̂ used to size this call's tables */
+  double ratio_observed;     /* max over waves of distinct / windows */
+  /* per-stage device milliseconds (timing=1): */
+  double ms_h2d, ms_supermer, ms_shuffle, ms_count, ms_compact, ms_overflow, ms_total;
+  /* host reader (step a) wall milliseconds */
+  double ms_reader;
+  uint32_t launches_count, launches_compact, launches_total;
+} gerbil_stats;
+
+/* Fills cfg with defaults (struct_size set, everything else "auto"). */
+void gerbil_config_default(gerbil_config* cfg);
+
+/* Creates a context on cfg->device. world > 1 requires nccl_unique_id (from
+ * gerbil_nccl_unique_id on rank 0, broadcast by the caller). */
+gerbil_status gerbil_init(const gerbil_config* cfg, gerbil_ctx** out);
+
+/* Writes a fresh ncclUniqueId (128 bytes) into id_out. */
+gerbil_status gerbil_nccl_unique_id(void* id_out, size_t id_len);
+
+/* Full path (a)→(e): host reader parses FASTA/FASTQ (PAPER.md:94-95,
+ * §2.3.1 steps 1-2), packs 2 bits/base, copies to the device, then counts.
+ * Validation: 8 <= k <= 200 (PAPER.md:447 allows 8..479; this build stops at
+ * 200), 1 <= m <= min(k-1, 15) or m == 0 (auto = 7),
+ * min_count >= 1, exactly one read source. */
+gerbil_status gerbil_count(gerbil_ctx* ctx, const gerbil_reads* reads,
+                           uint32_t k, uint32_t m, uint32_t min_count);
+
+/* Steps (b)→(e) on a packed batch already resident on this rank's device
+ * (layout above; nmask may be NULL when no base is undetermined). The
+ * headline timed region. n_reads may be 0. */
+gerbil_status gerbil_count_device(gerbil_ctx* ctx, const uint64_t* d_codes,
+                                  const uint64_t* d_nmask,
+                                  const uint64_t* d_read_start, uint64_t n_reads,
+                                  uint32_t k, uint32_t m, uint32_t min_count);
+
+/* Same as gerbil_count_device but from HOST buffers (the H2D copy is part of
+ * the call). Host buffers should be pinned for full PCIe bandwidth. */
+gerbil_status gerbil_count_host_packed(gerbil_ctx* ctx, const uint64_t* codes,
+                                       const uint64_t* nmask,
+                                       const uint64_t* read_start, uint64_t n_reads,
+                                       uint32_t k, uint32_t m, uint32_t min_count);
+
+/* Host reader alone (step a): parse FASTA/FASTQ and pack. Two-call pattern:
+ * with codes == NULL, returns the sizes (n_bases, n_reads) only. Buffers:
+ * codes[ceil(n_bases/32)], nmask[ceil(n_bases/64)], read_start[n_reads+1]. */
+gerbil_status gerbil_pack_reads(const gerbil_reads* reads, int32_t threads,
+                                uint64_t* codes, uint64_t* nmask,
+                                uint64_t* read_start, uint64_t* n_bases,
+                                uint64_t* n_reads, char* err, size_t err_len);
+
+/* Copies this rank's results (count >= min_count) into kmers[n*W] and
+ * counts[n]. kmers == NULL → only *n_out is written (two-call pattern).
+ * capacity is in entries. sorted != 0 → ascending key order (A<C<G<T).
+ * Fails with GERBIL_E_USAGE if capacity < n. */
+gerbil_status gerbil_fetch(gerbil_ctx* ctx, uint64_t* kmers, uint32_t* counts,
+                           uint64_t capacity, uint64_t* n_out, int sorted);
+
+/* Device-side view of this rank's results (valid until the next count). */
+gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers,
+                                    const uint32_t** d_counts, uint64_t* n,
+                                    uint32_t* W);
+
+gerbil_status gerbil_get_stats(const gerbil_ctx* ctx, gerbil_stats* out);
+const char* gerbil_last_error(const gerbil_ctx* ctx);
+void gerbil_finalize(gerbil_ctx* ctx);
+
+/* ---- debug / test entry points (step b in isolation) ------------------- */
+/* Runs step (b) only and copies the super-mers to host: pos[i] = base offset
+ * of the first window, nwin[i] = number of windows, bin[i], minimizer key
+ * mu[i] (ordering key of the canonical minimizer). Two-call
+ * pattern with pos == NULL. Order of super-mers is unspecified. */
+gerbil_status gerbil_debug_supermers(gerbil_ctx* ctx, const uint64_t* codes,
+                                     const uint64_t* nmask,
+                                     const uint64_t* read_start, uint64_t n_reads,
+                                     uint32_t k, uint32_t m, uint64_t* pos,
+                                     uint32_t* nwin, uint32_t* bin, uint32_t* mu,
+                                     uint64_t capacity, uint64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GERBIL_H */

@@ -17,7 +17,7 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(_PATH):
-            raise ImportError(f"{_PATH} missing; run paper_1607_06618_b200/_build.py")
+            raise ImportError(f"{_PATH} missing; run build_native.py")
         L = C.CDLL(_PATH)
         P = C.c_void_p
         L.oracle_count.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_char_p, C.c_uint64]

@@ -1,0 +1,880 @@
+// api.cu — C ABI (include/gerbil.h) and host orchestration of steps (a)-(e).
+//
+// One context = one rank = one GPU. gerbil_count_device runs, on the
+// context's stream:
+//   (b) supermer kernel → descriptors + per-bin histogram     (supermer.cu)
+//   [host] read the histogram; world > 1: all-gather it, assign bins to
+//          owner ranks (LPT), pack + NCCL all-to-all          (comm.cu)
+//   (c) bin scatter: descriptors grouped by bin                (shuffle.cu)
+//   [host] plan table waves (groups of bins whose table fits the budget)
+//   (d)+(e) per wave: count kernel, compaction kernel          (count.cu, compact.cu)
+//   emergency pass for overflowed k-mers; Σ-count invariant check.
+// Table waves reuse one table buffer sized to stay L2-resident
+// (cfg.wave_table_bytes, default 64 MiB of the 126 MB L2), so the hash-table
+// atomics are served by L2 and HBM sees the streaming traffic only.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gerbil.h"
+#include "comm.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "reader.h"
+
+using namespace gerbil;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    release();
+    size_t want = std::max<size_t>(n + n / 8, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      want = std::max<size_t>(n, 256);
+      e = cudaMalloc(&p, want);
+    }
+    if (e == cudaSuccess) bytes = want;
+    else p = nullptr;
+    return e;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// Device-side counters, zeroed per pass, read back once.
+struct Counters {
+  unsigned long long n_supermers, n_windows, ovf_n, out_n, sum_counts, distinct;
+  unsigned long long probe[4];
+};
+
+enum Kind { K_SUPERMER, K_SHUFFLE, K_COUNT, K_COMPACT, K_OVERFLOW, K_H2D, K_NKIND };
+
+struct TimedEvent {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+struct Wave {
+  uint64_t d0, d1;   // descriptor range (bin-ordered)
+  uint64_t windows;
+  uint64_t nb;       // buckets
+};
+
+}  // namespace
+
+struct gerbil_ctx {
+  gerbil_config cfg;
+  int device = 0, sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool poisoned = false;
+  std::string err;
+  double rho = 0.5;
+  Comm* comm = nullptr;
+  int rank = 0, world = 1;
+  // device buffers
+  DevBuf in_codes, in_nmask, in_rstart;  // uploads of host batches
+  DevBuf desc_pre, bin_pre, mu_dbg, desc_sorted;
+  DevBuf counters;
+  DevBuf hist;  // [3][B] windows, super-mers, payload words (ull)
+  DevBuf hist_all, cursor, cursor2, seg_base;
+  DevBuf table, ovf, out_keys, out_counts, wave_distinct;
+  DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
+  Counters* h_counters = nullptr;  // pinned
+  // results
+  bool have_result = false;
+  uint64_t n_out = 0;
+  uint32_t W = 0, k = 0;
+  gerbil_stats stats;
+  // timing
+  std::vector<TimedEvent> evs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+};
+
+namespace {
+
+gerbil_status fail(gerbil_ctx* c, gerbil_status st, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (st == GERBIL_E_CUDA || st == GERBIL_E_NCCL) c->poisoned = true;
+  }
+  return st;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ctx, GERBIL_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKS(expr)                              \
+  do {                                         \
+    gerbil_status s_ = (expr);                 \
+    if (s_ != GERBIL_OK) return s_;            \
+  } while (0)
+
+cudaEvent_t get_event(gerbil_ctx* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
+
+struct Timer {  // CUDA-event pair around one launch when timing is on
+  gerbil_ctx* ctx;
+  cudaEvent_t b = nullptr;
+  Timer(gerbil_ctx* c, int kind) : ctx(c) {
+    if (ctx->cfg.timing) {
+      cudaEvent_t a = get_event(ctx);
+      b = get_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+      ctx->evs.push_back({kind, a, b});
+    }
+  }
+  ~Timer() {
+    if (b) cudaEventRecord(b, ctx->stream);
+  }
+};
+
+gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_count) {
+  if (!ctx) return GERBIL_E_USAGE;
+  if (ctx->poisoned) return fail(ctx, GERBIL_E_STATE, "context poisoned by an earlier CUDA/NCCL error");
+  if (k < 8 || k > 200) return fail(ctx, GERBIL_E_USAGE, "k must be in [8, 200]");
+  if (m == 0) m = std::min<uint32_t>(7, k - 1);
+  if (m > 15 || m >= k) return fail(ctx, GERBIL_E_USAGE, "m must be in [1, min(k-1, 15)]");
+  if (min_count < 1) return fail(ctx, GERBIL_E_USAGE, "min_count must be >= 1");
+  return GERBIL_OK;
+}
+
+uint32_t choose_bins(const gerbil_ctx* ctx, uint64_t n_bases, uint32_t W) {
+  if (ctx->cfg.n_bins) return ctx->cfg.n_bins;
+  // Enough bins that one L2-sized wave packs ~16 of them (waves are unions of
+  // whole bins), at least 512 (the paper's default F) and at
+  // least 64 per rank.
+  const double slot = 8.0 + 8.0 * W;
+  const double table = ctx->rho * (double)n_bases * ctx->world * slot / ctx->cfg.target_load;
+  const double per_bin = (double)ctx->cfg.wave_table_bytes / 16.0;
+  uint32_t B = 512;
+  while ((double)B * per_bin < table && B < 8192) B <<= 1;
+  while (B < 64u * (uint32_t)ctx->world) B <<= 1;
+  return B;
+}
+
+double wall_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+// ---------------------------------------------------------------------------
+// Steps (d)+(e) over the bin-ordered descriptors of this rank.
+gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
+                          const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
+                          const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
+                          uint64_t total_windows) {
+  const uint32_t W = key_words(k);
+  const uint64_t bb = bucket_bytes(W);
+  const double slot_bytes = (double)bb / kSlotsPerBucket;
+  const double alpha = ctx->cfg.target_load;
+  const uint32_t theta = ctx->cfg.max_probes;
+  Counters& hc = *ctx->h_counters;
+  for (int attempt = 0;; ++attempt) {
+    const double rho = ctx->rho;
+    // plan waves: consecutive owned bins until the table budget is reached
+    std::vector<Wave> waves;
+    uint64_t max_nb = 1, out_bound = 0;
+    {
+      double acc = 0;
+      Wave cur{0, 0, 0, 0};
+      bool open = false;
+      auto close = [&] {
+        if (!open) return;
+        const double slots = std::max(64.0, std::ceil(rho * (double)cur.windows / alpha));
+        cur.nb = (uint64_t)std::ceil(slots / kSlotsPerBucket);
+        max_nb = std::max(max_nb, cur.nb);
+        out_bound += std::min<uint64_t>(cur.nb * kSlotsPerBucket, cur.windows);
+        waves.push_back(cur);
+        open = false;
+        acc = 0;
+      };
+      for (uint32_t b : bins) {
+        const double need = rho * (double)bin_win[b] / alpha * slot_bytes;
+        if (open && acc + need > (double)ctx->cfg.wave_table_bytes) close();
+        if (!open) {
+          cur = Wave{bin_off[b], bin_off[b], 0, 0};
+          open = true;
+        }
+        cur.d1 = bin_off[b + 1] - bin_off[b] + cur.d1;
+        cur.windows += bin_win[b];
+        acc += need;
+      }
+      close();
+    }
+    const uint64_t ovf_cap = std::max<uint64_t>(1 << 16, total_windows / 32);
+    CK(ctx->table.ensure(max_nb * bb));
+    CK(ctx->ovf.ensure(ovf_cap * W * 8));
+    const uint64_t out_cap = out_bound + ovf_cap;
+    CK(ctx->out_keys.ensure(out_cap * W * 8));
+    CK(ctx->out_counts.ensure(out_cap * 4));
+    CK(ctx->wave_distinct.ensure(std::max<size_t>(waves.size(), 1) * 8));
+    CK(cudaMemsetAsync(ctx->table.p, 0, max_nb * bb, ctx->stream));
+    CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, std::max<size_t>(waves.size(), 1) * 8, ctx->stream));
+    Counters* dc = ctx->counters.as<Counters>();
+    CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
+
+    TableArgs t{};
+    t.table = ctx->table.as<unsigned char>();
+    t.max_probes = theta;
+    t.ovf = ctx->ovf.as<uint64_t>();
+    t.ovf_cap = ovf_cap;
+    t.ovf_n = &dc->ovf_n;
+    t.probe_hist = dc->probe;
+    CompactArgs ca{};
+    ca.table = t.table;
+    ca.W = W;
+    ca.min_count = min_count;
+    ca.out_keys = ctx->out_keys.as<uint64_t>();
+    ca.out_counts = ctx->out_counts.as<uint32_t>();
+    ca.cap = out_cap;
+    ca.out_n = &dc->out_n;
+    ca.sum_counts = &dc->sum_counts;
+    ca.distinct = &dc->distinct;
+    for (size_t w = 0; w < waves.size(); ++w) {
+      t.nb = waves[w].nb;
+      CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t};
+      {
+        Timer tm(ctx, K_COUNT);
+        CK(launch_count(a, W, ctx->sms, ctx->stream));
+      }
+      ca.nb = waves[w].nb;
+      ca.wave_distinct = ctx->wave_distinct.as<unsigned long long>() + w;
+      {
+        Timer tm(ctx, K_COMPACT);
+        CK(launch_compact(ca, ctx->sms, ctx->stream));
+      }
+    }
+    CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<unsigned long long> wd(waves.size());
+    if (!waves.empty())
+      CK(cudaMemcpyAsync(wd.data(), ctx->wave_distinct.p, waves.size() * 8, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double observed = 0;
+    for (size_t w = 0; w < waves.size(); ++w)
+      if (waves[w].windows) observed = std::max(observed, (double)wd[w] / (double)waves[w].windows);
+    ctx->stats.waves = (uint32_t)waves.size();
+    ctx->stats.ratio_used = rho;
+    ctx->stats.ratio_observed = observed;
+    ctx->stats.overflow_kmers = hc.ovf_n;
+    ctx->stats.overflow_passes = 0;
+    ctx->stats.probe_first = hc.probe[0];
+    ctx->stats.probe_more = hc.probe[1];
+    ctx->stats.probe_max = hc.probe[2];
+    const uint64_t ovf_n = hc.ovf_n;
+    if (ovf_n > ovf_cap) {
+      // emergency area exhausted: redo the waves with larger tables
+      ctx->rho = std::min(1.0, std::max(2.0 * rho, 1.25 * observed + 0.02));
+      if (attempt > 8) return fail(ctx, GERBIL_E_INTERNAL, "table sizing did not converge");
+      continue;
+    }
+    if (ovf_n > 0) {
+      // emergency mechanism: count the overflowed k-mers
+      // exactly in a table with room for all of them and θ = every bucket.
+      const uint64_t nb2 = std::max<uint64_t>(8, (uint64_t)std::ceil((double)ovf_n / (0.5 * kSlotsPerBucket)));
+      CK(ctx->table.ensure(nb2 * bb));
+      CK(cudaMemsetAsync(ctx->table.p, 0, nb2 * bb, ctx->stream));
+      // overflow keys must not be overwritten while re-inserted: θ = nb2 never overflows
+      TableArgs t2 = t;
+      t2.table = ctx->table.as<unsigned char>();
+      t2.nb = nb2;
+      t2.max_probes = (uint32_t)std::min<uint64_t>(nb2, 0xffffffffu);
+      t2.ovf_cap = 0;
+      CountKeysArgs ka{ctx->ovf.as<uint64_t>(), ovf_n, k, t2};
+      {
+        Timer tm(ctx, K_OVERFLOW);
+        CK(launch_count_keys(ka, W, ctx->sms, ctx->stream));
+      }
+      CompactArgs c2 = ca;
+      c2.table = t2.table;
+      c2.nb = nb2;
+      c2.wave_distinct = nullptr;
+      {
+        Timer tm(ctx, K_OVERFLOW);
+        CK(launch_compact(c2, ctx->sms, ctx->stream));
+      }
+      CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->stats.overflow_passes = 1;
+      if (hc.ovf_n != ovf_n) return fail(ctx, GERBIL_E_INTERNAL, "emergency pass overflowed");
+    }
+    if (hc.out_n > out_cap) return fail(ctx, GERBIL_E_INTERNAL, "result buffer bound violated");
+    // ratio adaptation for the next call ("we dynamically adjust the ratio")
+    if (observed > 0) ctx->rho = std::min(1.0, std::max(observed * 1.15 + 0.01, 0.02));
+    ctx->n_out = hc.out_n;
+    ctx->stats.kept = hc.out_n;
+    ctx->stats.distinct = hc.distinct;
+    ctx->stats.count_sum = hc.sum_counts;
+    ctx->stats.owned_windows = total_windows;
+    ctx->stats.launches_count = 0;
+    return GERBIL_OK;
+  }
+}
+
+// ---------------------------------------------------------------------------
+gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                           const uint64_t* rstart, uint64_t n_reads, uint64_t n_bases, uint32_t k,
+                           uint32_t m, uint32_t B, bool want_mu, uint64_t& n_sm) {
+  const uint32_t w = k - m + 1;
+  uint64_t cap = (uint64_t)((double)n_bases * 2.0 / (w + 1) * 1.3) + (n_bases / kTile + 1) * 4 + 1024;
+  Counters* dc = ctx->counters.as<Counters>();
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CK(ctx->desc_pre.ensure(cap * 8));
+    CK(ctx->bin_pre.ensure(cap * 4));
+    if (want_mu) CK(ctx->mu_dbg.ensure(cap * 4));
+    CK(cudaMemsetAsync(dc, 0, sizeof(Counters), ctx->stream));
+    CK(cudaMemsetAsync(ctx->hist.p, 0, 3ull * B * 8, ctx->stream));
+    SupermerArgs a{};
+    a.codes = codes;
+    a.nmask = nmask;
+    a.read_start = rstart;
+    a.n_reads = n_reads;
+    a.n_bases = n_bases;
+    a.k = k;
+    a.m = m;
+    a.n_bins = B;
+    a.ordering = (uint32_t)ctx->cfg.ordering;
+    a.desc = ctx->desc_pre.as<uint64_t>();
+    a.bin = ctx->bin_pre.as<uint32_t>();
+    a.mu = want_mu ? ctx->mu_dbg.as<uint32_t>() : nullptr;
+    a.cap = cap;
+    a.n_supermers = &dc->n_supermers;
+    a.n_windows = &dc->n_windows;
+    unsigned long long* h = ctx->hist.as<unsigned long long>();
+    a.bin_windows = h;
+    a.bin_supermers = h + B;
+    a.bin_words = ctx->world > 1 ? h + 2 * B : nullptr;
+    {
+      Timer tm(ctx, K_SUPERMER);
+      CK(launch_supermer(a, ctx->sms, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    n_sm = ctx->h_counters->n_supermers;
+    if (n_sm <= cap) return GERBIL_OK;
+    cap = n_sm + 1024;
+  }
+  return fail(ctx, GERBIL_E_INTERNAL, "super-mer buffer sizing did not converge");
+}
+
+gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                uint32_t min_count) {
+  const double t0 = wall_ms();
+  ctx->have_result = false;
+  ctx->n_out = 0;
+  ctx->evs.clear();
+  ctx->ev_used = 0;
+  memset(&ctx->stats, 0, sizeof ctx->stats);
+  const uint32_t W = key_words(k);
+  ctx->W = W;
+  ctx->k = k;
+  uint64_t n_bases = 0;
+  if (n_reads > 0) {
+    CK(cudaMemcpyAsync(&ctx->h_counters->probe[3], rstart + n_reads, 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    n_bases = ctx->h_counters->probe[3];
+  }
+  // all ranks must agree on B: derive it from the largest local batch
+  uint64_t nb_for_bins = n_bases;
+  const uint32_t B = choose_bins(ctx, nb_for_bins, W);
+  if (ctx->world > 1 && ctx->cfg.n_bins == 0)
+    return fail(ctx, GERBIL_E_USAGE, "world > 1 requires an explicit n_bins (identical on all ranks)");
+  CK(ctx->counters.ensure(sizeof(Counters)));
+  CK(ctx->hist.ensure(3ull * B * 8));
+  ctx->stats.n_bins = B;
+  ctx->stats.W = W;
+  ctx->stats.input_bases = n_bases;
+  ctx->stats.input_reads = n_reads;
+
+  // (b)
+  uint64_t n_sm = 0;
+  CKS(run_supermer(ctx, codes, nmask, rstart, n_reads, n_bases, k, m, B, false, n_sm));
+  const uint64_t local_windows = ctx->h_counters->n_windows;
+  ctx->stats.supermers = n_sm;
+  ctx->stats.valid_windows = local_windows;
+  std::vector<unsigned long long> hist(3ull * B);
+  CK(cudaMemcpyAsync(hist.data(), ctx->hist.p, 3ull * B * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+
+  std::vector<uint64_t> bin_win(B), bin_off(B + 1, 0);
+  std::vector<uint32_t> owned;
+  const uint64_t* stream_codes = codes;
+  uint64_t owned_windows = 0;
+  if (ctx->world <= 1) {
+    // (c) local: group descriptors by bin
+    for (uint32_t b = 0; b < B; ++b) {
+      bin_win[b] = hist[b];
+      bin_off[b + 1] = bin_off[b] + hist[B + b];
+      owned.push_back(b);
+      owned_windows += hist[b];
+    }
+    ctx->stats.max_bin_windows = *std::max_element(bin_win.begin(), bin_win.end());
+    CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n_sm, 1) * 8));
+    CK(ctx->cursor.ensure((size_t)B * 8));
+    CK(cudaMemcpyAsync(ctx->cursor.p, bin_off.data(), (size_t)B * 8, cudaMemcpyHostToDevice, ctx->stream));
+    ScatterArgs s{};
+    s.desc_in = ctx->desc_pre.as<uint64_t>();
+    s.bin_in = ctx->bin_pre.as<uint32_t>();
+    s.n = n_sm;
+    s.n_bins = B;
+    s.cursor = ctx->cursor.as<unsigned long long>();
+    s.desc_out = ctx->desc_sorted.as<uint64_t>();
+    {
+      Timer tm(ctx, K_SHUFFLE);
+      CK(launch_scatter(s, ctx->sms, ctx->stream));
+    }
+  } else {
+    // (c) multi-GPU: all-gather histograms, LPT owners, pack, all-to-all, regroup
+    const int P = ctx->world, r = ctx->rank;
+    CK(ctx->hist_all.ensure(3ull * B * 8 * P));
+    if (!ctx->comm->allgather(ctx->hist.p, ctx->hist_all.p, 3ull * B * 8, ctx->stream))
+      return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+    std::vector<unsigned long long> H(3ull * B * P);
+    CK(cudaMemcpyAsync(H.data(), ctx->hist_all.p, H.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    auto Hw = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + b]; };
+    auto Hc = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + B + b]; };
+    auto Hp = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + 2 * B + b]; };
+    std::vector<uint64_t> gw(B, 0);
+    for (int s = 0; s < P; ++s)
+      for (uint32_t b = 0; b < B; ++b) gw[b] += Hw(s, b);
+    ctx->stats.max_bin_windows = *std::max_element(gw.begin(), gw.end());
+    // LPT: heaviest bin first to the least-loaded rank (ties → lower rank/bin)
+    std::vector<uint32_t> order(B);
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return gw[a] > gw[b]; });
+    std::vector<int> owner(B);
+    std::vector<uint64_t> load(P, 0);
+    for (uint32_t b : order) {
+      int best = 0;
+      for (int p = 1; p < P; ++p)
+        if (load[p] < load[best]) best = p;
+      owner[b] = best;
+      load[best] += gw[b];
+    }
+    // send layout ordered by (dest, bin)
+    std::vector<uint64_t> sd_off(P + 1, 0), sw_off(P + 1, 0);
+    std::vector<unsigned long long> cur_d(B), cur_w(B), seg(B);
+    for (int d = 0; d < P; ++d) {
+      uint64_t cd = sd_off[d], cw = sw_off[d];
+      for (uint32_t b = 0; b < B; ++b)
+        if (owner[b] == d) {
+          cur_d[b] = cd;
+          cur_w[b] = cw;
+          seg[b] = sw_off[d];
+          cd += Hc(r, b);
+          cw += Hp(r, b);
+        }
+      sd_off[d + 1] = cd;
+      sw_off[d + 1] = cw;
+    }
+    // receive layout: source-major; inside a source, owned bins in bin order
+    std::vector<uint64_t> rd_off(P + 1, 0), rw_off(P + 1, 0);
+    for (int s = 0; s < P; ++s) {
+      uint64_t cd = 0, cw = 0;
+      for (uint32_t b = 0; b < B; ++b)
+        if (owner[b] == r) {
+          cd += Hc(s, b);
+          cw += Hp(s, b);
+        }
+      rd_off[s + 1] = rd_off[s] + cd;
+      rw_off[s + 1] = rw_off[s] + cw;
+    }
+    const uint64_t n_send = sd_off[P], w_send = sw_off[P], n_recv = rd_off[P], w_recv = rw_off[P];
+    CK(ctx->send_desc.ensure(std::max<uint64_t>(n_send, 1) * 8));
+    CK(ctx->send_bin.ensure(std::max<uint64_t>(n_send, 1) * 4));
+    CK(ctx->send_payload.ensure(std::max<uint64_t>(w_send, 1) * 8));
+    CK(ctx->recv_desc.ensure(std::max<uint64_t>(n_recv, 1) * 8));
+    CK(ctx->recv_bin.ensure(std::max<uint64_t>(n_recv, 1) * 4));
+    CK(ctx->recv_payload.ensure(std::max<uint64_t>(w_recv, 1) * 8));
+    CK(ctx->cursor.ensure((size_t)B * 8));
+    CK(ctx->cursor2.ensure((size_t)B * 8));
+    CK(ctx->seg_base.ensure((size_t)B * 8));
+    CK(cudaMemcpyAsync(ctx->cursor.p, cur_d.data(), (size_t)B * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->cursor2.p, cur_w.data(), (size_t)B * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->seg_base.p, seg.data(), (size_t)B * 8, cudaMemcpyHostToDevice, ctx->stream));
+    PackArgs pa{};
+    pa.desc_in = ctx->desc_pre.as<uint64_t>();
+    pa.bin_in = ctx->bin_pre.as<uint32_t>();
+    pa.n = n_sm;
+    pa.codes = codes;
+    pa.k = k;
+    pa.cur_desc = ctx->cursor.as<unsigned long long>();
+    pa.cur_words = ctx->cursor2.as<unsigned long long>();
+    pa.seg_word_base = ctx->seg_base.as<unsigned long long>();
+    pa.send_desc = ctx->send_desc.as<uint64_t>();
+    pa.send_bin = ctx->send_bin.as<uint32_t>();
+    pa.send_payload = ctx->send_payload.as<uint64_t>();
+    {
+      Timer tm(ctx, K_SHUFFLE);
+      CK(launch_pack(pa, ctx->sms, ctx->stream));
+    }
+    std::vector<size_t> so(P), sb(P), ro(P), rb(P);
+    auto xchg = [&](const DevBuf& sbuf, const std::vector<uint64_t>& soff, DevBuf& rbuf,
+                    const std::vector<uint64_t>& roff, size_t elem) {
+      for (int p = 0; p < P; ++p) {
+        so[p] = soff[p] * elem;
+        sb[p] = (soff[p + 1] - soff[p]) * elem;
+        ro[p] = roff[p] * elem;
+        rb[p] = (roff[p + 1] - roff[p]) * elem;
+      }
+      return ctx->comm->alltoallv(sbuf.p, so.data(), sb.data(), rbuf.p, ro.data(), rb.data(), ctx->stream);
+    };
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!xchg(ctx->send_desc, sd_off, ctx->recv_desc, rd_off, 8) ||
+        !xchg(ctx->send_bin, sd_off, ctx->recv_bin, rd_off, 4) ||
+        !xchg(ctx->send_payload, sw_off, ctx->recv_payload, rw_off, 8))
+      return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+    ctx->stats.bytes_sent = (n_send - (sd_off[r + 1] - sd_off[r])) * 12 + (w_send - (sw_off[r + 1] - sw_off[r])) * 8;
+    ctx->stats.bytes_recv = (n_recv - (rd_off[r + 1] - rd_off[r])) * 12 + (w_recv - (rw_off[r + 1] - rw_off[r])) * 8;
+    // regroup received descriptors by bin, rebasing pos into recv_payload
+    for (uint32_t b = 0; b < B; ++b) {
+      uint64_t c = 0, wv = 0;
+      if (owner[b] == r)
+        for (int s = 0; s < P; ++s) {
+          c += Hc(s, b);
+          wv += Hw(s, b);
+        }
+      bin_off[b + 1] = bin_off[b] + c;
+      bin_win[b] = wv;
+      if (owner[b] == r) {
+        owned.push_back(b);
+        owned_windows += wv;
+      }
+    }
+    CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n_recv, 1) * 8));
+    CK(cudaMemcpyAsync(ctx->cursor.p, bin_off.data(), (size_t)B * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (int s = 0; s < P; ++s) {
+      ScatterArgs sa{};
+      sa.desc_in = ctx->recv_desc.as<uint64_t>() + rd_off[s];
+      sa.bin_in = ctx->recv_bin.as<uint32_t>() + rd_off[s];
+      sa.n = rd_off[s + 1] - rd_off[s];
+      sa.n_bins = B;
+      sa.cursor = ctx->cursor.as<unsigned long long>();
+      sa.desc_out = ctx->desc_sorted.as<uint64_t>();
+      sa.pos_add = rw_off[s] * 32;
+      Timer tm(ctx, K_SHUFFLE);
+      CK(launch_scatter(sa, ctx->sms, ctx->stream));
+    }
+    stream_codes = ctx->recv_payload.as<uint64_t>();
+  }
+
+  // (d) + (e)
+  CKS(count_waves(ctx, stream_codes, ctx->desc_sorted.as<uint64_t>(), bin_off, bin_win, owned, k,
+                  min_count, owned_windows));
+  // Σ-count invariant: every valid window counted exactly once
+  if (ctx->stats.count_sum != owned_windows)
+    return fail(ctx, GERBIL_E_INTERNAL,
+                "invariant violated: sum of counts " + std::to_string(ctx->stats.count_sum) +
+                    " != valid windows " + std::to_string(owned_windows));
+  // timing
+  if (ctx->cfg.timing) {
+    double ms[K_NKIND] = {0};
+    uint32_t n[K_NKIND] = {0};
+    for (auto& e : ctx->evs) {
+      float f = 0;
+      cudaEventElapsedTime(&f, e.a, e.b);
+      ms[e.kind] += f;
+      n[e.kind]++;
+    }
+    ctx->stats.ms_supermer = ms[K_SUPERMER];
+    ctx->stats.ms_shuffle = ms[K_SHUFFLE];
+    ctx->stats.ms_count = ms[K_COUNT];
+    ctx->stats.ms_compact = ms[K_COMPACT];
+    ctx->stats.ms_overflow = ms[K_OVERFLOW];
+    ctx->stats.launches_count = n[K_COUNT];
+    ctx->stats.launches_compact = n[K_COMPACT];
+    uint32_t tot = 0;
+    for (int i = 0; i < K_NKIND; ++i) tot += n[i];
+    ctx->stats.launches_total = tot;
+  }
+  ctx->stats.ms_total = wall_ms() - t0;
+  ctx->have_result = true;
+  return GERBIL_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI =====
+extern "C" {
+
+void gerbil_config_default(gerbil_config* cfg) {
+  memset(cfg, 0, sizeof *cfg);
+  cfg->struct_size = sizeof *cfg;
+  cfg->device = -1;
+  cfg->world = 1;
+}
+
+gerbil_status gerbil_nccl_unique_id(void* id_out, size_t id_len) {
+  if (!id_out || id_len < 128) return GERBIL_E_USAGE;
+  std::string err;
+  return nccl_get_unique_id(id_out, err) ? GERBIL_OK : GERBIL_E_NCCL;
+}
+
+gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
+  if (!cfg_in || !out) return GERBIL_E_USAGE;
+  *out = nullptr;
+  gerbil_config cfg;
+  gerbil_config_default(&cfg);
+  memcpy(&cfg, cfg_in, std::min<size_t>(cfg_in->struct_size ? cfg_in->struct_size : sizeof cfg, sizeof cfg));
+  cfg.struct_size = sizeof cfg;
+  if (cfg.world < 1) cfg.world = 1;
+  if (cfg.rank < 0 || cfg.rank >= cfg.world) return GERBIL_E_USAGE;
+  if (cfg.world > 1 && !cfg.nccl_unique_id) return GERBIL_E_USAGE;
+  if (cfg.n_bins > (1u << 20)) return GERBIL_E_USAGE;
+  if (cfg.max_probes == 0) cfg.max_probes = 32;
+  if (cfg.target_load <= 0) cfg.target_load = 0.7;
+  if (cfg.target_load > 4.0) return GERBIL_E_USAGE;
+  if (cfg.distinct_ratio < 0 || cfg.distinct_ratio > 1) return GERBIL_E_USAGE;
+  if (cfg.wave_table_bytes == 0) cfg.wave_table_bytes = 64ull << 20;
+  gerbil_ctx* ctx = new gerbil_ctx();
+  ctx->cfg = cfg;
+  ctx->rho = cfg.distinct_ratio > 0 ? cfg.distinct_ratio : 0.5;
+  ctx->rank = cfg.rank;
+  ctx->world = cfg.world;
+  cudaError_t e = cudaSuccess;
+  if (cfg.device >= 0) e = cudaSetDevice(cfg.device);
+  if (e == cudaSuccess) e = cudaGetDevice(&ctx->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  if (e == cudaSuccess) {
+    if (cfg.stream) {
+      ctx->stream = (cudaStream_t)cfg.stream;
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_counters, sizeof(Counters));
+  if (e != cudaSuccess) {
+    delete ctx;
+    return GERBIL_E_CUDA;
+  }
+  if (cfg.world > 1) {
+    std::string err;
+    ctx->comm = make_comm(cfg.comm_backend, cfg.nccl_unique_id, cfg.rank, cfg.world, err);
+    if (!ctx->comm) {
+      gerbil_finalize(ctx);
+      return GERBIL_E_NCCL;
+    }
+  }
+  *out = ctx;
+  return GERBIL_OK;
+}
+
+void gerbil_finalize(gerbil_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  delete ctx->comm;
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* gerbil_last_error(const gerbil_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+gerbil_status gerbil_get_stats(const gerbil_ctx* ctx, gerbil_stats* out) {
+  if (!ctx || !out) return GERBIL_E_USAGE;
+  *out = ctx->stats;
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_count_device(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                  const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                  uint32_t min_count) {
+  CKS(validate(ctx, k, m, min_count));
+  if (n_reads > 0 && (!codes || !rstart)) return fail(ctx, GERBIL_E_USAGE, "null device buffer");
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, GERBIL_E_CUDA, "cudaSetDevice");
+  return count_device_impl(ctx, codes, nmask, rstart, n_reads, k, m, min_count);
+}
+
+gerbil_status gerbil_count_host_packed(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                       const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                       uint32_t min_count) {
+  CKS(validate(ctx, k, m, min_count));
+  if (!rstart) return fail(ctx, GERBIL_E_USAGE, "null host buffer");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t nb = rstart[n_reads];
+  if (nb > 0 && !codes) return fail(ctx, GERBIL_E_USAGE, "null host buffer");
+  const uint64_t ncw = std::max<uint64_t>((nb + 31) / 32, 1), nmw = std::max<uint64_t>((nb + 63) / 64, 1);
+  CK(ctx->in_codes.ensure(ncw * 8));
+  CK(ctx->in_nmask.ensure(nmw * 8));
+  CK(ctx->in_rstart.ensure((n_reads + 1) * 8));
+  {
+    Timer tm(ctx, K_H2D);
+    CK(cudaMemcpyAsync(ctx->in_codes.p, codes, ((nb + 31) / 32) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (nmask)
+      CK(cudaMemcpyAsync(ctx->in_nmask.p, nmask, ((nb + 63) / 64) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->in_rstart.p, rstart, (n_reads + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return count_device_impl(ctx, ctx->in_codes.as<uint64_t>(), nmask ? ctx->in_nmask.as<uint64_t>() : nullptr,
+                           ctx->in_rstart.as<uint64_t>(), n_reads, k, m, min_count);
+}
+
+gerbil_status gerbil_pack_reads(const gerbil_reads* reads, int32_t threads, uint64_t* codes,
+                                uint64_t* nmask, uint64_t* rstart, uint64_t* n_bases, uint64_t* n_reads,
+                                char* err, size_t err_len) {
+  if (!reads || !n_bases || !n_reads) return GERBIL_E_USAGE;
+  const bool has_text = reads->text != nullptr, has_paths = reads->paths != nullptr && reads->n_paths > 0;
+  if (has_text == has_paths) return GERBIL_E_USAGE;
+  PackedBatch pb;
+  std::string e;
+  bool ok = true;
+  if (has_text) ok = pack_text(reads->text, reads->text_len, threads, pb, e, "<memory>");
+  else
+    for (uint32_t i = 0; ok && i < reads->n_paths; ++i) ok = pack_file(reads->paths[i], threads, pb, e);
+  if (!ok) {
+    if (err && err_len) {
+      strncpy(err, e.c_str(), err_len - 1);
+      err[err_len - 1] = 0;
+    }
+    return GERBIL_E_IO;
+  }
+  if (pb.read_start.empty()) pb.read_start.push_back(0);
+  *n_bases = pb.n_bases;
+  *n_reads = pb.n_reads;
+  if (codes) {
+    memcpy(codes, pb.codes.data(), pb.codes.size() * 8);
+    if (nmask) memcpy(nmask, pb.nmask.data(), pb.nmask.size() * 8);
+    if (rstart) memcpy(rstart, pb.read_start.data(), pb.read_start.size() * 8);
+  }
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_count(gerbil_ctx* ctx, const gerbil_reads* reads, uint32_t k, uint32_t m,
+                           uint32_t min_count) {
+  CKS(validate(ctx, k, m, min_count));
+  if (!reads) return fail(ctx, GERBIL_E_USAGE, "null reads");
+  const bool has_text = reads->text != nullptr, has_paths = reads->paths != nullptr && reads->n_paths > 0;
+  if (has_text == has_paths) return fail(ctx, GERBIL_E_USAGE, "exactly one read source must be set");
+  const double t0 = wall_ms();
+  PackedBatch pb;
+  std::string e;
+  bool ok = true;
+  if (has_text) ok = pack_text(reads->text, reads->text_len, ctx->cfg.host_threads, pb, e, "<memory>");
+  else
+    for (uint32_t i = 0; ok && i < reads->n_paths; ++i) ok = pack_file(reads->paths[i], ctx->cfg.host_threads, pb, e);
+  if (!ok) return fail(ctx, GERBIL_E_IO, e);
+  if (pb.read_start.empty()) pb.read_start.push_back(0);
+  const double t_reader = wall_ms() - t0;
+  gerbil_status st = gerbil_count_host_packed(ctx, pb.codes.data(), pb.nmask.data(), pb.read_start.data(),
+                                              pb.n_reads, k, m, min_count);
+  ctx->stats.ms_reader = t_reader;
+  return st;
+}
+
+gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers, const uint32_t** d_counts,
+                                    uint64_t* n, uint32_t* W) {
+  if (!ctx) return GERBIL_E_USAGE;
+  if (!ctx->have_result) return fail(ctx, GERBIL_E_STATE, "no successful count yet");
+  if (d_kmers) *d_kmers = ctx->out_keys.as<uint64_t>();
+  if (d_counts) *d_counts = ctx->out_counts.as<uint32_t>();
+  if (n) *n = ctx->n_out;
+  if (W) *W = ctx->W;
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_fetch(gerbil_ctx* ctx, uint64_t* kmers, uint32_t* counts, uint64_t capacity,
+                           uint64_t* n_out, int sorted) {
+  if (!ctx || !n_out) return GERBIL_E_USAGE;
+  if (!ctx->have_result) return fail(ctx, GERBIL_E_STATE, "no successful count yet");
+  *n_out = ctx->n_out;
+  if (!kmers) return GERBIL_OK;
+  if (capacity < ctx->n_out) return fail(ctx, GERBIL_E_USAGE, "capacity too small");
+  const uint64_t n = ctx->n_out, W = ctx->W;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(kmers, ctx->out_keys.p, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (counts) CK(cudaMemcpyAsync(counts, ctx->out_counts.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (sorted && n > 1) {
+    std::vector<uint64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0ull);
+    std::sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
+      return std::lexicographical_compare(kmers + a * W, kmers + a * W + W, kmers + b * W, kmers + b * W + W);
+    });
+    std::vector<uint64_t> kk(n * W);
+    std::vector<uint32_t> cc(counts ? n : 0);
+    for (uint64_t i = 0; i < n; ++i) {
+      memcpy(&kk[i * W], kmers + idx[i] * W, W * 8);
+      if (counts) cc[i] = counts[idx[i]];
+    }
+    memcpy(kmers, kk.data(), n * W * 8);
+    if (counts) memcpy(counts, cc.data(), n * 4);
+  }
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_debug_supermers(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                     const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                     uint64_t* pos, uint32_t* nwin, uint32_t* bin, uint32_t* mu,
+                                     uint64_t capacity, uint64_t* n_out) {
+  // step (b) alone accepts the small k of the paper's Fig. 1 example (k=4, m=3)
+  if (!ctx) return GERBIL_E_USAGE;
+  if (k < 2 || k > 200 || m < 1 || m >= k || m > 15)
+    return fail(ctx, GERBIL_E_USAGE, "debug_supermers: need 2 <= k <= 200, 1 <= m < k, m <= 15");
+  if (!rstart || !n_out) return fail(ctx, GERBIL_E_USAGE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  // host buffers in, like gerbil_count_host_packed
+  const uint64_t nb = rstart[n_reads];
+  CK(ctx->in_codes.ensure(std::max<uint64_t>((nb + 31) / 32, 1) * 8));
+  CK(ctx->in_nmask.ensure(std::max<uint64_t>((nb + 63) / 64, 1) * 8));
+  CK(ctx->in_rstart.ensure((n_reads + 1) * 8));
+  CK(cudaMemcpy(ctx->in_codes.p, codes, ((nb + 31) / 32) * 8, cudaMemcpyHostToDevice));
+  if (nmask) CK(cudaMemcpy(ctx->in_nmask.p, nmask, ((nb + 63) / 64) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->in_rstart.p, rstart, (n_reads + 1) * 8, cudaMemcpyHostToDevice));
+  const uint32_t B = ctx->cfg.n_bins ? ctx->cfg.n_bins : 512;
+  CK(ctx->counters.ensure(sizeof(Counters)));
+  CK(ctx->hist.ensure(3ull * B * 8));
+  uint64_t n_sm = 0;
+  CKS(run_supermer(ctx, ctx->in_codes.as<uint64_t>(), nmask ? ctx->in_nmask.as<uint64_t>() : nullptr,
+                   ctx->in_rstart.as<uint64_t>(), n_reads, nb, k, m, B, true, n_sm));
+  *n_out = n_sm;
+  if (!pos) return GERBIL_OK;
+  if (capacity < n_sm) return fail(ctx, GERBIL_E_USAGE, "capacity too small");
+  std::vector<uint64_t> d(n_sm);
+  CK(cudaMemcpy(d.data(), ctx->desc_pre.p, n_sm * 8, cudaMemcpyDeviceToHost));
+  if (bin) CK(cudaMemcpy(bin, ctx->bin_pre.p, n_sm * 4, cudaMemcpyDeviceToHost));
+  if (mu) CK(cudaMemcpy(mu, ctx->mu_dbg.p, n_sm * 4, cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < n_sm; ++i) {
+    pos[i] = d[i] >> kNwinBits;
+    if (nwin) nwin[i] = (uint32_t)(d[i] & ((1u << kNwinBits) - 1)) + 1;
+  }
+  return GERBIL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+// comm.cu — NCCL (dlopen) and loopback implementations of Comm.
+//
+// The bin shuffle is the path's only partition point: an
+// all-gather of the per-bin histograms, then a grouped ncclSend/ncclRecv
+// all-to-allv of super-mer descriptors and payload over NVLink 5 / NVSwitch.
+// NCCL is loaded at run time (the process may already hold torch's copy of
+// libnccl.so.2; RTLD_NOLOAD picks that one first).
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "comm.h"
+
+namespace gerbil {
+namespace {
+
+// ---------------------------------------------------------------- NCCL ----
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+NcclApi* nccl_api(std::string& err) {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define SYM(n) api.n = reinterpret_cast<decltype(api.n)>(dlsym(h, "nccl" #n))
+    SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(AllGather); SYM(Send);
+    SYM(Recv); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString);
+#undef SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
+             api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+  });
+  if (!api.ok) {
+    err = "libnccl.so.2 could not be loaded";
+    return nullptr;
+  }
+  return &api;
+}
+
+class NcclComm : public Comm {
+ public:
+  NcclApi* api = nullptr;
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) api->CommDestroy(comm);
+  }
+  bool check(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return true;
+    err = std::string(what) + ": " + api->GetErrorString(r);
+    return false;
+  }
+  bool allgather(const void* s, void* r, size_t bytes, cudaStream_t st) override {
+    if (!check(api->AllGather(s, r, bytes, ncclUint8, comm, st), "ncclAllGather")) return false;
+    return cudaStreamSynchronize(st) == cudaSuccess;
+  }
+  bool alltoallv(const void* s, const size_t* so, const size_t* sb, void* r, const size_t* ro,
+                 const size_t* rb, cudaStream_t st) override {
+    if (!check(api->GroupStart(), "ncclGroupStart")) return false;
+    for (int p = 0; p < world; ++p) {
+      if (sb[p] && !check(api->Send((const char*)s + so[p], sb[p], ncclUint8, p, comm, st), "ncclSend"))
+        return false;
+      if (rb[p] && !check(api->Recv((char*)r + ro[p], rb[p], ncclUint8, p, comm, st), "ncclRecv"))
+        return false;
+    }
+    if (!check(api->GroupEnd(), "ncclGroupEnd")) return false;
+    return cudaStreamSynchronize(st) == cudaSuccess;
+  }
+};
+
+// ------------------------------------------------------------ loopback ----
+struct LoopGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned gen = 0;
+  std::vector<const void*> send;
+  std::vector<const size_t*> soff, sbytes;
+  explicit LoopGroup(int w) : world(w), send(w), soff(w), sbytes(w) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    unsigned g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+std::mutex g_reg_mu;
+std::map<std::string, std::weak_ptr<LoopGroup>> g_registry;
+
+class LoopComm : public Comm {
+ public:
+  std::shared_ptr<LoopGroup> g;
+  bool allgather(const void* s, void* r, size_t bytes, cudaStream_t st) override {
+    g->send[rank] = s;
+    g->barrier();
+    bool ok = true;
+    for (int p = 0; p < world; ++p)
+      ok &= cudaMemcpyAsync((char*)r + p * bytes, g->send[p], bytes, cudaMemcpyDeviceToDevice, st) ==
+            cudaSuccess;
+    ok &= cudaStreamSynchronize(st) == cudaSuccess;
+    g->barrier();
+    if (!ok) err = "loopback allgather copy failed";
+    return ok;
+  }
+  bool alltoallv(const void* s, const size_t* so, const size_t* sb, void* r, const size_t* ro,
+                 const size_t* rb, cudaStream_t st) override {
+    g->send[rank] = s;
+    g->soff[rank] = so;
+    g->sbytes[rank] = sb;
+    g->barrier();
+    bool ok = true;
+    for (int p = 0; p < world; ++p) {
+      size_t n = g->sbytes[p][rank];
+      if (n != rb[p]) ok = false;
+      if (n && ok)
+        ok &= cudaMemcpyAsync((char*)r + ro[p], (const char*)g->send[p] + g->soff[p][rank], n,
+                              cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+    }
+    ok &= cudaStreamSynchronize(st) == cudaSuccess;
+    g->barrier();
+    if (!ok) err = "loopback alltoallv size mismatch or copy failure";
+    return ok;
+  }
+};
+
+}  // namespace
+
+Comm* make_comm(int backend, const void* id, int rank, int world, std::string& err) {
+  if (backend == 1) {
+    std::string key((const char*)id, 128);
+    std::shared_ptr<LoopGroup> g;
+    {
+      std::lock_guard<std::mutex> lk(g_reg_mu);
+      auto it = g_registry.find(key);
+      if (it != g_registry.end()) g = it->second.lock();
+      if (!g) {
+        g = std::make_shared<LoopGroup>(world);
+        g_registry[key] = g;
+      }
+    }
+    if (g->world != world) {
+      err = "loopback group world size mismatch";
+      return nullptr;
+    }
+    LoopComm* c = new LoopComm();
+    c->g = g;
+    c->rank = rank;
+    c->world = world;
+    return c;
+  }
+  NcclApi* api = nccl_api(err);
+  if (!api) return nullptr;
+  NcclComm* c = new NcclComm();
+  c->api = api;
+  c->rank = rank;
+  c->world = world;
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, sizeof uid.internal);
+  ncclResult_t r = api->CommInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    err = std::string("ncclCommInitRank: ") + api->GetErrorString(r);
+    c->comm = nullptr;
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+bool nccl_get_unique_id(void* out, std::string& err) {
+  NcclApi* api = nccl_api(err);
+  if (!api) return false;
+  ncclUniqueId uid;
+  ncclResult_t r = api->GetUniqueId(&uid);
+  if (r != ncclSuccess) {
+    err = std::string("ncclGetUniqueId: ") + api->GetErrorString(r);
+    return false;
+  }
+  memcpy(out, uid.internal, sizeof uid.internal);
+  return true;
+}
+
+}  // namespace gerbil

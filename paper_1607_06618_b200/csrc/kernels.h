@@ -1,0 +1,103 @@
+// kernels.h — launch wrappers of the device steps (b)-(e); internal to the
+// library (the public boundary is include/gerbil.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gerbil {
+
+struct SupermerArgs {
+  const uint64_t* codes;       // packed 2-bit stream
+  const uint64_t* nmask;       // N bitmap or nullptr
+  const uint64_t* read_start;  // n_reads + 1 base offsets
+  uint64_t n_reads;
+  uint64_t n_bases;            // read_start[n_reads]
+  uint32_t k, m, n_bins, ordering;
+  uint32_t k_bits_for_words;   // k (payload words per super-mer = ceil((nwin+k-1)/32))
+  // outputs
+  uint64_t* desc;              // [cap] pos << 11 | (nwin - 1)
+  uint32_t* bin;               // [cap]
+  uint32_t* mu;                // [cap] minimizer key (debug) or nullptr
+  uint64_t cap;
+  unsigned long long* n_supermers;   // total produced (may exceed cap → caller regrows)
+  unsigned long long* n_windows;     // Σ nwin (valid windows)
+  unsigned long long* bin_windows;   // [n_bins]
+  unsigned long long* bin_supermers; // [n_bins]
+  unsigned long long* bin_words;     // [n_bins] payload words (multi-GPU) or nullptr
+};
+cudaError_t launch_supermer(const SupermerArgs& a, int sms, cudaStream_t s);
+
+struct ScatterArgs {
+  const uint64_t* desc_in;
+  const uint32_t* bin_in;
+  uint64_t n;
+  uint32_t n_bins;
+  unsigned long long* cursor;  // [n_bins], initialised to the bin offsets
+  uint64_t* desc_out;
+  uint32_t* bin_out;           // optional (nullptr)
+  uint64_t pos_add;            // added to pos (rebasing received super-mers)
+  const unsigned char* keep;   // optional per-bin filter (owned bins) or nullptr
+};
+cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t s);
+
+// world > 1: copy every local super-mer (descriptor + word-aligned payload)
+// into the send buffer, ordered by (destination rank, bin).
+struct PackArgs {
+  const uint64_t* desc_in;
+  const uint32_t* bin_in;
+  uint64_t n;
+  const uint64_t* codes;
+  uint32_t k;
+  unsigned long long* cur_desc;              // [B] next send slot of the bin
+  unsigned long long* cur_words;             // [B] next payload word of the bin
+  const unsigned long long* seg_word_base;   // [B] first payload word of the bin's destination
+  uint64_t* send_desc;
+  uint32_t* send_bin;
+  uint64_t* send_payload;
+};
+cudaError_t launch_pack(const PackArgs& a, int sms, cudaStream_t s);
+
+struct TableArgs {
+  unsigned char* table;  // nb buckets
+  uint64_t nb;
+  uint32_t max_probes;   // θ (buckets)
+  uint64_t* ovf;         // overflow keys [ovf_cap * W]
+  uint64_t ovf_cap;
+  unsigned long long* ovf_n;
+  unsigned long long* probe_hist;  // [4]: first-bucket hits, >1 bucket, max probes, unused
+};
+
+struct CountArgs {
+  const uint64_t* codes;   // stream the descriptors point into
+  const uint64_t* desc;    // bin-ordered descriptors
+  uint64_t d0, d1;         // wave range
+  uint32_t k;
+  TableArgs t;
+};
+cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
+
+struct CountKeysArgs {      // emergency path: insert overflow keys
+  const uint64_t* keys;     // [n * W]
+  uint64_t n;
+  uint32_t k;
+  TableArgs t;
+};
+cudaError_t launch_count_keys(const CountKeysArgs& a, uint32_t W, int sms, cudaStream_t s);
+
+struct CompactArgs {
+  unsigned char* table;
+  uint64_t nb;
+  uint32_t W, min_count;
+  uint64_t* out_keys;      // [cap * W]
+  uint32_t* out_counts;    // [cap]
+  uint64_t cap;
+  unsigned long long* out_n;
+  unsigned long long* sum_counts;
+  unsigned long long* distinct;
+  unsigned long long* wave_distinct;  // per-wave slot or nullptr
+};
+cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t s);
+
+cudaError_t launch_clear_table(unsigned char* table, uint64_t bytes, int sms, cudaStream_t s);
+
+}  // namespace gerbil

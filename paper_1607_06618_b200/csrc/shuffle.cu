@@ -1,0 +1,137 @@
+// shuffle.cu — step (c), local part: group super-mer descriptors by bin.
+//
+// PAPER.md:49 ("all occurrences of a certain k-mer are stored in the same
+// temporary file") and :97 (single writer fills the temporary files). Here the
+// "files" are bin-contiguous ranges of a descriptor array in HBM: a counting
+// sort with per-bin cursors pre-set to the bin offsets (exclusive scan of the
+// per-bin super-mer counts from step (b)). Each CTA ranks its chunk inside
+// shared memory and reserves one global range per (CTA chunk, bin), so global
+// atomics scale with distinct bins per chunk, not with super-mers. Order
+// inside a bin is unspecified (counting is order-insensitive).
+// For world > 1 the same kernel regroups received descriptors (pos_add
+// rebases them into the receive buffer) and builds the per-destination send
+// order (bin index = dest * n_bins + bin, see api.cu).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gerbil {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPer = 8;
+constexpr int kChunk = kThreads * kPer;
+
+__global__ void __launch_bounds__(kThreads)
+scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
+  extern __shared__ uint32_t s_mem[];
+  uint32_t* s_cnt = s_mem;                                   // [n_bins]
+  unsigned long long* s_base = (unsigned long long*)(s_mem + ((a.n_bins + 1) & ~1u));
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t b = tid; b < a.n_bins; b += kThreads) s_cnt[b] = 0;
+  __syncthreads();
+  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint64_t i0 = c * kChunk;
+    uint32_t bins[kPer], rank[kPer];
+    uint64_t desc[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint64_t i = i0 + j * kThreads + tid;
+      bins[j] = 0xffffffffu;
+      if (i < a.n) {
+        const uint32_t b = a.bin_in[i];
+        if (!a.keep || a.keep[b]) {
+          bins[j] = b;
+          desc[j] = a.desc_in[i];
+          rank[j] = atomicAdd(&s_cnt[b], 1u);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (bins[j] != 0xffffffffu && rank[j] == 0)
+        s_base[bins[j]] = atomicAdd(&a.cursor[bins[j]], (unsigned long long)s_cnt[bins[j]]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (bins[j] != 0xffffffffu) {
+        const uint64_t d = s_base[bins[j]] + rank[j];
+        a.desc_out[d] = desc[j] + (a.pos_add << kNwinBits);
+        if (a.bin_out) a.bin_out[d] = bins[j];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (bins[j] != 0xffffffffu && rank[j] == 0) s_cnt[bins[j]] = 0;
+    __syncthreads();
+  }
+}
+
+__global__ void scatter_global_kernel(ScatterArgs a) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = a.bin_in[i];
+    if (a.keep && !a.keep[b]) continue;
+    const uint64_t d = atomicAdd(&a.cursor[b], 1ull);
+    a.desc_out[d] = a.desc_in[i] + (a.pos_add << kNwinBits);
+    if (a.bin_out) a.bin_out[d] = b;
+  }
+}
+
+__global__ void pack_kernel(PackArgs a) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = a.desc_in[i];
+    const uint32_t b = a.bin_in[i];
+    const uint64_t pos = d >> kNwinBits;
+    const uint32_t nwin = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
+    const uint64_t L = nwin + a.k - 1;
+    const uint32_t nw = (uint32_t)((L + 31) / 32);
+    const uint64_t j = atomicAdd(&a.cur_desc[b], 1ull);
+    const uint64_t wo = atomicAdd(&a.cur_words[b], (unsigned long long)nw);
+    a.send_desc[j] = (((wo - a.seg_word_base[b]) * 32) << kNwinBits) | (nwin - 1);
+    a.send_bin[j] = b;
+    for (uint32_t t = 0; t < nw; ++t) {
+      const uint64_t q = pos + 32ull * t;
+      const uint64_t e = (q + 32 < pos + L) ? q + 32 : pos + L;  // bases [q, e)
+      const uint64_t w0 = q >> 5;
+      const uint32_t s = (uint32_t)(q & 31) * 2;
+      const uint64_t hi = __ldg(a.codes + w0);
+      const uint64_t lo = (((e - 1) >> 5) > w0) ? __ldg(a.codes + w0 + 1) : 0ull;
+      uint64_t v = s ? ((hi << s) | (lo >> (64 - s))) : hi;
+      const uint32_t nb = (uint32_t)(e - q);
+      if (nb < 32) v &= ~0ull << (64 - 2 * nb);
+      a.send_payload[wo + t] = v;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const PackArgs& a, int sms, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  pack_kernel<<<sms * 8, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  if (a.n_bins <= 16384) {
+    const size_t dyn = (size_t)((a.n_bins + 1) & ~1u) * 4 + (size_t)a.n_bins * 8;
+    cudaError_t e = cudaFuncSetAttribute(scatter_smem_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scatter_smem_kernel, kThreads, dyn);
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t n_chunks = (a.n + kChunk - 1) / kChunk;
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (grid > n_chunks) grid = n_chunks;
+    scatter_smem_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, n_chunks);
+  } else {
+    scatter_global_kernel<<<sms * 8, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace gerbil

@@ -34,7 +34,7 @@ def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(_PATH):
-            raise ImportError(f"{_PATH} missing; run paper_1607_06618_b200/_build.py")
+            raise ImportError(f"{_PATH} missing; run build_native.py")
         L = C.CDLL(_PATH)
         L.synth_fastx.argtypes = [C.POINTER(Params), C.c_int, C.c_uint32, C.c_void_p, C.c_uint64, C.c_int]
         L.synth_fastx.restype = C.c_uint64

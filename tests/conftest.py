@@ -12,7 +12,7 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running full-size parity")
     # incremental native build (no-op when up to date); nvcc cross-compiles without a GPU
-    from paper_1607_06618_b200 import _build
+    import build_native as _build
 
     _build.build_all()
 

@@ -1,0 +1,120 @@
+"""CPU-only checks of the boundary: the C-ABI library loads and exports every
+symbol include/gerbil.h declares; the host reader (step a) packs exactly what
+the text says; the seeded generator is deterministic and its packed twin
+matches its ASCII output. No compute call needs a GPU here."""
+import ctypes
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from tests.helpers import decode_packed
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "gerbil.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gerbil_[a-z_]+)\s*\(", src)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_1607_06618_b200 import gerbil
+
+    lib = ctypes.CDLL(gerbil.library_path())
+    declared = _declared_symbols()
+    assert "gerbil_count" in declared and "gerbil_fetch" in declared and "gerbil_init" in declared
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/gerbil.h but not exported"
+    assert sorted(gerbil.EXPORTED) == declared
+
+
+def test_product_does_not_import_oracle():
+    # the product path must never route through the oracle
+    for dirpath, _, files in os.walk(os.path.join(ROOT, "paper_1607_06618_b200")):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                txt = open(os.path.join(dirpath, f), errors="replace").read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "liboracle" not in txt, f
+
+
+def _texts(reads):
+    fa = b"".join(b">r%d\n" % i + r + b"\n" for i, r in enumerate(reads))
+    fa_ml = b"".join(b">r%d\n" % i + b"\n".join(r[j:j + 13] for j in range(0, len(r), 13)) + b"\n"
+                     for i, r in enumerate(reads))
+    fq = b"".join(b"@r%d\n" % i + r + b"\n+\n" + b"I" * len(r) + b"\n" for i, r in enumerate(reads))
+    return [fa, fa_ml, fq, fa.replace(b"\n", b"\r\n"), b"".join(r + b"\n" for r in reads if r)]
+
+
+def test_reader_packs_exactly():
+    from paper_1607_06618_b200 import gerbil
+
+    rnd = random.Random(1)
+    reads = [bytes(rnd.choice(b"ACGTacgtNnRY.") for _ in range(rnd.randint(1, 150))) for _ in range(97)]
+    for t in _texts(reads):
+        for threads in (1, 3, 8):
+            p = gerbil.pack_reads(text=t, threads=threads)
+            assert p.n_reads == len(reads)
+            assert p.n_bases == sum(len(r) for r in reads)
+            for i, r in enumerate(reads):
+                s, e = int(p.read_start[i]), int(p.read_start[i + 1])
+                expect = bytes(c if c in b"ACGT" else ord("N") for c in r.upper())
+                assert decode_packed(p.codes, p.nmask, s, e - s) == expect
+
+
+def test_reader_empty_and_errors(tmp_path):
+    from paper_1607_06618_b200 import gerbil
+
+    p = gerbil.pack_reads(text=b"")
+    assert p.n_reads == 0 and p.n_bases == 0
+    with pytest.raises(gerbil.GerbilError):
+        gerbil.pack_reads(text=b"@r\nACGT\n-\nIIII\n")
+    with pytest.raises(gerbil.GerbilError):
+        gerbil.pack_reads(text=b"@r\nACGT\n+\nIII\n")
+    with pytest.raises(gerbil.GerbilError):
+        gerbil.pack_reads(paths=[str(tmp_path / "missing.fa")])
+    f1, f2 = tmp_path / "a.fa", tmp_path / "b.fq"
+    f1.write_bytes(b">x\nACGTACGTAC\n")
+    f2.write_bytes(b"@y\nGGGNNTTT\n+\nIIIIIIII\n")
+    p = gerbil.pack_reads(paths=[str(f1), str(f2)])
+    assert p.n_reads == 2 and list(p.read_start) == [0, 10, 18]
+    assert decode_packed(p.codes, p.nmask, 0, 18) == b"ACGTACGTACGGGNNTTT"
+
+
+def test_synth_deterministic_and_shardable():
+    w = synth.Workload(seed=5, genome_len=50_000, read_len=100, n_reads=300, err=0.01, nrate=0.002)
+    a, b = synth.fastx(w, synth.RAW), synth.fastx(w, synth.RAW)
+    assert a == b
+    lines = a.split(b"\n")[:-1]
+    assert len(lines) == 300 and all(len(l) == 100 for l in lines)
+    s0, s1 = w.shard(0, 2), w.shard(1, 2)
+    assert synth.fastx(s0, synth.RAW) + synth.fastx(s1, synth.RAW) == a
+    # N rate and substitution rate roughly as requested
+    n_frac = a.count(b"N") / 30000
+    assert 0 < n_frac < 0.01
+    w2 = synth.Workload(seed=6, genome_len=50_000, read_len=100, n_reads=300)
+    assert synth.fastx(w2, synth.RAW) != synth.fastx(w, synth.RAW)
+
+
+def test_synth_packed_twin_matches_ascii():
+    w = synth.Workload(seed=3, genome_len=20_000, read_len=77, n_reads=211, err=0.02, nrate=0.01)
+    codes, nmask, rs = synth.packed_host(w, threads=4)
+    text = synth.fastx(w, synth.RAW).split(b"\n")[:-1]
+    assert list(rs) == [i * 77 for i in range(212)]
+    for i, r in enumerate(text):
+        assert decode_packed(codes, nmask, i * 77, 77) == r
+
+
+def test_reader_matches_synth_packing():
+    from paper_1607_06618_b200 import gerbil
+
+    w = synth.Workload(seed=9, genome_len=30_000, read_len=100, n_reads=500, err=0.01, nrate=0.003)
+    codes, nmask, rs = synth.packed_host(w)
+    p = gerbil.pack_reads(text=synth.fastx(w, synth.FASTQ))
+    assert np.array_equal(p.read_start, rs)
+    assert np.array_equal(p.codes[: len(codes)], codes)
+    assert np.array_equal(p.nmask[: len(nmask)], nmask)
