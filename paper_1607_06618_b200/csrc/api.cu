@@ -29,6 +29,8 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "reader.h"
+#include "table.cuh"
+#include "table_inline.cuh"
 
 using namespace gerbil;
 
@@ -93,7 +95,7 @@ struct gerbil_ctx {
   int rank = 0, world = 1;
   // device buffers
   DevBuf in_codes, in_nmask, in_rstart;  // uploads of host batches
-  DevBuf desc_pre, bin_pre, mu_dbg, desc_sorted;
+  DevBuf desc_pre, bin_pre, mu_dbg, desc_sorted, tile_first;
   DevBuf counters;
   DevBuf hist;  // [3][B] windows, super-mers, payload words (ull)
   DevBuf hist_all, cursor, cursor2, seg_base;
@@ -196,7 +198,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
                           const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
                           uint64_t total_windows) {
   const uint32_t W = key_words(k);
-  const uint64_t bb = bucket_bytes(W);
+  const uint64_t bb = table_inline(k) ? kInlineBucketBytes : table_bucket_bytes(k);
   const double slot_bytes = (double)bb / kSlotsPerBucket;
   const double alpha = ctx->cfg.target_load;
   const uint32_t theta = ctx->cfg.max_probes;
@@ -239,9 +241,11 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     const uint64_t out_cap = out_bound + ovf_cap;
     CK(ctx->out_keys.ensure(out_cap * W * 8));
     CK(ctx->out_counts.ensure(out_cap * 4));
-    CK(ctx->wave_distinct.ensure(std::max<size_t>(waves.size(), 1) * 8));
+    // [0, n): distinct per wave; [n, 2n): dynamic work counters of the count launches
+    const size_t nw = std::max<size_t>(waves.size(), 1);
+    CK(ctx->wave_distinct.ensure(2 * nw * 8));
     CK(cudaMemsetAsync(ctx->table.p, 0, max_nb * bb, ctx->stream));
-    CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, std::max<size_t>(waves.size(), 1) * 8, ctx->stream));
+    CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, 2 * nw * 8, ctx->stream));
     Counters* dc = ctx->counters.as<Counters>();
     CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
 
@@ -254,7 +258,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     t.probe_hist = dc->probe;
     CompactArgs ca{};
     ca.table = t.table;
-    ca.W = W;
+    ca.k = k;
     ca.min_count = min_count;
     ca.out_keys = ctx->out_keys.as<uint64_t>();
     ca.out_counts = ctx->out_counts.as<uint32_t>();
@@ -264,7 +268,8 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ca.distinct = &dc->distinct;
     for (size_t w = 0; w < waves.size(); ++w) {
       t.nb = waves[w].nb;
-      CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t};
+      CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t,
+                  ctx->wave_distinct.as<unsigned long long>() + nw + w};
       {
         Timer tm(ctx, K_COUNT);
         CK(launch_count(a, W, ctx->sms, ctx->stream));
@@ -282,9 +287,20 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
       CK(cudaMemcpyAsync(wd.data(), ctx->wave_distinct.p, waves.size() * 8, cudaMemcpyDeviceToHost,
                          ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    // observed distinct/total ratio: max over waves large enough to be a fair
+    // sample (a tiny wave of a few singletons would read 1.0 and bloat every
+    // table of the next call); small inputs fall back to the pooled ratio
     double observed = 0;
+    uint64_t big = 0, pooled_w = 0, pooled_d = 0;
+    for (size_t w = 0; w < waves.size(); ++w) {
+      big = std::max(big, waves[w].windows);
+      pooled_w += waves[w].windows;
+      pooled_d += wd[w];
+    }
     for (size_t w = 0; w < waves.size(); ++w)
-      if (waves[w].windows) observed = std::max(observed, (double)wd[w] / (double)waves[w].windows);
+      if (waves[w].windows >= std::max<uint64_t>(big / 4, 1))
+        observed = std::max(observed, (double)wd[w] / (double)waves[w].windows);
+    if (pooled_w) observed = std::max(observed, (double)pooled_d / (double)pooled_w);
     ctx->stats.waves = (uint32_t)waves.size();
     ctx->stats.ratio_used = rho;
     ctx->stats.ratio_observed = observed;
@@ -376,9 +392,10 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     a.bin_windows = h;
     a.bin_supermers = h + B;
     a.bin_words = ctx->world > 1 ? h + 2 * B : nullptr;
+    CK(ctx->tile_first.ensure(std::max<uint64_t>(supermer_tiles(n_bases), 1) * 8));
     {
       Timer tm(ctx, K_SUPERMER);
-      CK(launch_supermer(a, ctx->sms, ctx->stream));
+      CK(launch_supermer(a, ctx->tile_first.as<uint64_t>(), ctx->sms, ctx->stream));
     }
     CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -10,7 +10,7 @@
 namespace gerbil {
 
 constexpr int kMaxW = 7;          // k <= 200 → W = ceil(k/32) <= 7
-constexpr uint32_t kSlotsPerBucket = 8;
+constexpr uint32_t kSlotsPerBucket = 4;  // table.cuh bucket layout
 constexpr uint32_t kReady = 0x80000000u;
 constexpr uint32_t kFpMask = 0x7fffffffu;
 constexpr int kNwinBits = 11;     // super-mer descriptor: pos << 11 | (nwin-1)
@@ -18,8 +18,6 @@ constexpr uint32_t kTile = 2048;  // window positions per step-(b) tile (= max s
 
 __host__ __device__ inline uint32_t key_words(uint32_t k) { return (k + 31) / 32; }
 
-// Bucket = [8 × u32 tag][8 × u32 count][8 × W × u64 key].
-__host__ __device__ inline uint64_t bucket_bytes(uint32_t W) { return 64 + 64ull * W; }
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t h) {
   h ^= h >> 33;

@@ -5,58 +5,106 @@
 // output buffer"; PAPER.md:467 (`-l count`): "the minimal occurrence of a
 // k-mer to be outputted" (reading Q5: output iff count >= min_count).
 //
-// One thread per slot; keepers are appended to the SoA result with one
-// atomic per warp (ballot + popc). The same pass sums every count (Σ-count
+// Each CTA iteration covers 1024 slots (4 per thread). Keepers are ranked
+// with warp ballots and one global atomic per CTA iteration reserves their
+// output range; keys are converted from table chunks back to the W-word
+// result layout (include/gerbil.h). The same pass sums every count (Σ-count
 // invariant), counts distinct keys, and clears the slots it
-// read, so the (L2-resident) table buffer is clean for the next wave without
-// a separate memset.
+// read, so the L2-resident table buffer is clean for the next wave.
 #include "common.cuh"
 #include "kernels.h"
+#include "table.cuh"
+#include "table_inline.cuh"
 
 namespace gerbil {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPer = 4;
 
 __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
-  const uint32_t lane = lane_id();
+  __shared__ uint32_t s_cnt[kWarps * kPer];
+  __shared__ unsigned long long s_base;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const uint32_t W = key_words(a.k);
+  const bool inl = table_inline(a.k);
+  const uint32_t WP = inl ? (a.k > 31 ? 2 : 1) : chunk_words(a.k);
   const uint64_t n_slots = a.nb * kSlotsPerBucket;
-  const uint64_t bb = bucket_bytes(a.W);
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   uint64_t my_sum = 0, my_distinct = 0;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads + (threadIdx.x & ~31u); base < n_slots;
-       base += stride) {
-    const uint64_t slot = base + lane;
-    uint32_t tag = 0, cnt = 0;
-    uint32_t* tags = nullptr;
-    if (slot < n_slots) {
-      unsigned char* bucket = a.table + (slot >> 3) * bb;
-      tags = reinterpret_cast<uint32_t*>(bucket) + (slot & 7);
-      tag = *tags;
-      if (tag) cnt = tags[kSlotsPerBucket];
+  for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kPer; base < n_slots;
+       base += (uint64_t)gridDim.x * kThreads * kPer) {
+    uint64_t c0[kPer], c1[kPer];
+    uint32_t cnt[kPer], rank[kPer];
+    bool keep[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const uint64_t slot = base + j * kThreads + tid;
+      c0[j] = 0;
+      c1[j] = 0;
+      cnt[j] = 0;
+      if (slot < n_slots) {
+        if (inl) {  // 16-byte slot {chunk0, chunk1 | count}
+          const uint64_t* p = reinterpret_cast<const uint64_t*>(a.table) + 2 * slot;
+          c0[j] = p[0];
+          c1[j] = p[1];
+          cnt[j] = (uint32_t)c1[j];
+        } else {
+          const Bucket bk = bucket_at(a.table, slot >> 2, WP);
+          c0[j] = bk.c0[slot & 3];
+          if (c0[j]) cnt[j] = bk.cnt[slot & 3];
+        }
+      }
+      keep[j] = c0[j] != 0 && cnt[j] >= a.min_count;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep[j]);
+      rank[j] = __popc(m & ((1u << lane) - 1u));
+      if (lane == 0) s_cnt[j * kWarps + warp] = __popc(m);
     }
-    const bool keep = tag != 0u && cnt >= a.min_count;
-    const uint32_t mask = __ballot_sync(0xffffffffu, keep);
-    unsigned long long out0 = 0;
-    if (mask) {
-      if (lane == 0) out0 = atomicAdd(a.out_n, (unsigned long long)__popc(mask));
-      out0 = __shfl_sync(0xffffffffu, out0, 0);
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (int i = 0; i < kWarps * kPer; ++i) {
+        const uint32_t v = s_cnt[i];
+        s_cnt[i] = run;
+        run += v;
+      }
+      s_base = run ? atomicAdd(a.out_n, (unsigned long long)run) : 0ull;
     }
-    if (keep) {
-      const uint64_t idx = out0 + __popc(mask & ((1u << lane) - 1u));
-      if (idx < a.cap) {
-        const uint64_t* key = reinterpret_cast<const uint64_t*>(
-            a.table + (slot >> 3) * bb + 64) + (slot & 7) * a.W;
-        for (uint32_t w = 0; w < a.W; ++w) a.out_keys[idx * a.W + w] = key[w];
-        a.out_counts[idx] = cnt;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      if (!c0[j]) continue;
+      const uint64_t slot = base + j * kThreads + tid;
+      const Bucket bk = bucket_at(a.table, slot >> 2, WP);
+      const uint32_t s = slot & 3;
+      if (keep[j]) {
+        const uint64_t idx = s_base + s_cnt[j * kWarps + warp] + rank[j];
+        if (idx < a.cap) {
+          uint64_t ch[8], key[kMaxW];
+          ch[0] = c0[j];
+          if (inl) {
+            ch[1] = c1[j] & 0xffffffff00000000ull;
+          } else {
+            for (uint32_t q = 1; q < WP; ++q) ch[q] = bk.rest[s * (WP - 1) + (q - 1)];
+          }
+          from_chunks(ch, WP, key, W);
+          for (uint32_t w = 0; w < W; ++w) a.out_keys[idx * W + w] = key[w];
+          a.out_counts[idx] = cnt[j];
+        }
+      }
+      my_sum += cnt[j];
+      ++my_distinct;
+      if (inl) {
+        uint64_t* p = reinterpret_cast<uint64_t*>(a.table) + 2 * slot;
+        p[0] = 0ull;
+        p[1] = 0ull;
+      } else {
+        bk.c0[s] = 0ull;
+        bk.cnt[s] = 0u;
+        for (uint32_t q = 1; q < WP; ++q) bk.rest[s * (WP - 1) + (q - 1)] = 0ull;
       }
     }
-    if (tag) {
-      my_sum += cnt;
-      ++my_distinct;
-      tags[0] = 0u;
-      tags[kSlotsPerBucket] = 0u;
-    }
+    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -75,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
 cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t st) {
   const uint64_t n_slots = a.nb * kSlotsPerBucket;
   if (n_slots == 0) return cudaSuccess;
-  uint64_t grid = (n_slots + kThreads - 1) / kThreads;
+  uint64_t grid = (n_slots + kThreads * kPer - 1) / (kThreads * kPer);
   if (grid > (uint64_t)sms * 8) grid = (uint64_t)sms * 8;
   compact_kernel<<<(unsigned)grid, kThreads, 0, st>>>(a);
   return cudaGetLastError();

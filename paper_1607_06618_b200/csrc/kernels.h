@@ -25,7 +25,9 @@ struct SupermerArgs {
   unsigned long long* bin_supermers; // [n_bins]
   unsigned long long* bin_words;     // [n_bins] payload words (multi-GPU) or nullptr
 };
-cudaError_t launch_supermer(const SupermerArgs& a, int sms, cudaStream_t s);
+// tile_first: scratch of supermer_tiles(n_bases) u64 entries.
+cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms, cudaStream_t s);
+uint64_t supermer_tiles(uint64_t n_bases);
 
 struct ScatterArgs {
   const uint64_t* desc_in;
@@ -73,6 +75,7 @@ struct CountArgs {
   uint64_t d0, d1;         // wave range
   uint32_t k;
   TableArgs t;
+  unsigned long long* work;  // zeroed per launch: dynamic chunk counter
 };
 cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
 
@@ -87,7 +90,7 @@ cudaError_t launch_count_keys(const CountKeysArgs& a, uint32_t W, int sms, cudaS
 struct CompactArgs {
   unsigned char* table;
   uint64_t nb;
-  uint32_t W, min_count;
+  uint32_t k, min_count;
   uint64_t* out_keys;      // [cap * W]
   uint32_t* out_counts;    // [cap]
   uint64_t cap;
