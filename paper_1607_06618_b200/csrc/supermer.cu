@@ -14,19 +14,20 @@
 //   0. tile_reads_kernel: first read of every tile (one pass over read_start);
 //   1. stage the tile's packed codes, N-mask and read starts in smem
 //      (bitmaps are LSB-first u32 words: position i = bit i%32 of word i/32);
-//   2. per position j: m-mer f_j, rc(f_j), ordering key
-//      c_j = min(ord f_j, ord rc f_j) (strand-symmetric minimizer, Q7);
-//   3. sliding minimum over w = k-m+1 keys by log2(w) doubling passes in smem
-//      (sparse table: min[p, p+w) = min(M_a[p], M_a[p+w-a]));
-//   4. window p valid iff its k bases are N-free and inside one read
-//      (PAPER.md:121-122): X = N | (read-start shifted by one); valid iff
-//      no X bit in [p, p+k-2] and base p+k-1 is not N — one next-set-bit scan;
-//   5. positions are strided over threads (p = i*256 + tid) so the valid and
-//      start bitmaps come straight out of warp ballots; a super-mer is a
-//      maximal run of valid windows with equal μ (value-based runs, DESIGN.md
-//      Q8), cut at tile boundaries; its length is the distance to the next
-//      break bit;
-//   6. bin = fastrange(fmix32(μ), B); descriptors are appended with one global
+//   2. keys: thread t rolls the m-mers of key block t (8 consecutive
+//      positions: one extraction, then 2-bit shifts of f and rc(f)); ordering
+//      key c_j = min(ord f_j, ord rc f_j) (strand-symmetric minimizer,
+//      DESIGN.md Q7); it publishes the block's prefix minima, suffix minima
+//      and minimum;
+//   3. thread t owns windows p = 8t..8t+7: μ_p = min over c[p, p+w) =
+//      min(suffix[p], min of the whole blocks in between, prefix[p+w-1]);
+//      validity: no X = N | RS(q+1) bit in [p, p+k-2] and
+//      base p+k-1 not N — one amortised next-set-bit scan per thread;
+//   4. a super-mer starts at a valid window whose predecessor is invalid or has
+//      another μ (value-based runs, Q8); the break bitmap is built
+//      with 4-lane shuffles; a super-mer's length is the distance to the next
+//      break (tile boundaries cut super-mers);
+//   5. bin = fastrange(fmix32(μ), B); descriptors are appended with one global
 //      atomic per tile; per-bin counts accumulate in smem and are flushed once
 //      per persistent CTA.
 #include "common.cuh"
@@ -39,9 +40,10 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPer = kTile / kThreads;  // 8 window positions per thread
 constexpr int kMaxK = 200;
-constexpr int kCodeWords = (kTile + kMaxK + 31) / 32 + 2;  // u64 words of 32 bases
+constexpr int kCodeWords = (kTile + kMaxK + 31) / 32 + 2;        // u64 words of 32 bases
 constexpr int kBitWords = ((kTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
-constexpr int kKeyLen = kTile + kMaxK;
+constexpr int kKeyLen = kTile + kMaxK;                           // >= kTile + k - m
+constexpr int kKeyBlocks = (kKeyLen + 7) / 8;
 
 __device__ __forceinline__ bool bget(const uint32_t* bm, uint32_t i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
 
@@ -77,6 +79,10 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t base_at(const uint64_t* codes, uint32_t j) {
+  return (uint32_t)(codes[j >> 5] >> (62 - 2 * (j & 31))) & 3u;
+}
+
 __global__ void tile_reads_kernel(const uint64_t* __restrict__ read_start, uint64_t n_reads,
                                   uint64_t n_tiles, uint64_t* __restrict__ tile_first) {
   // tile t starts at p0 = t*kTile; its first read is the last r with read_start[r] <= p0
@@ -88,26 +94,32 @@ __global__ void tile_reads_kernel(const uint64_t* __restrict__ read_start, uint6
   }
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_t n_tiles, int hist_smem) {
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
   __shared__ uint32_t s_rs[kBitWords];   // read-start bits
   __shared__ uint32_t s_x[kBitWords];    // N(q) | RS(q+1)
-  __shared__ uint32_t s_valid[kTile / 32];
+  __shared__ uint32_t s_key[kKeyLen];    // c_j
+  __shared__ uint32_t s_pre[kKeyLen];    // min over c[8b .. j] (j in block b)
+  __shared__ uint32_t s_suf[kKeyLen];    // min over c[j .. 8b+7]
+  __shared__ uint32_t s_blk[kKeyBlocks]; // min over block b
   __shared__ uint32_t s_brk[kTile / 32 + 1];
-  __shared__ uint32_t s_buf[2][kKeyLen];
+  __shared__ uint32_t s_last[kThreads];  // μ of window 8t+7, or ~0 if invalid
   __shared__ uint32_t s_warp[kWarps];
   __shared__ unsigned long long s_base;
-  extern __shared__ uint32_t s_hist[];  // [2 or 3][n_bins] when hist_smem
+  extern __shared__ uint32_t s_hist[];   // [2 or 3][n_bins] when hist_smem
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint32_t k = a.k, m = a.m, B = a.n_bins;
   const uint32_t w = k - m + 1;
   const uint32_t n_keys = kTile + k - m;  // m-mers needed by the tile's windows
+  const uint32_t n_blocks = (n_keys + 7) / 8;
   const uint32_t n_bits = kTile + k;      // staged base positions
   const uint64_t n_code_words = (a.n_bases + 31) / 32, n_mask_words = (a.n_bases + 63) / 64;
   const int nh = a.bin_words ? 3 : 2;
+  const uint32_t mmask = (uint32_t)((1ull << (2 * m)) - 1);
+  const uint64_t end_p = a.n_bases >= k ? a.n_bases - k + 1 : 0;  // windows start below this
   uint32_t* h_win = s_hist;
   uint32_t* h_cnt = s_hist + B;
   uint32_t* h_wrd = s_hist + 2 * B;
@@ -138,62 +150,110 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       if (v >= lim) break;
       if (v > p0) atomicOr(&s_rs[(uint32_t)(v - p0) >> 5], 1u << ((uint32_t)(v - p0) & 31));
     }
-    // 2. ordering keys of the strand-symmetric m-mers
-    const uint32_t sh_r = 64 - 2 * m;
-    const uint64_t mmask = (1ull << (2 * m)) - 1;
-    for (uint32_t j = tid; j < n_keys; j += kThreads) {
-      const uint32_t wi = j >> 5, sh = (j & 31) * 2;
+    // 2. rolling strand-symmetric m-mer keys, block prefix/suffix minima
+    for (uint32_t b = tid; b < n_blocks; b += kThreads) {
+      const uint32_t j0 = 8 * b;
+      // initial m-mer at j0
+      const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
       const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
-      const uint32_t f = (uint32_t)(v >> sh_r);
-      const uint32_t rc = (uint32_t)(rev_pairs(~v & (~0ull << sh_r)) & mmask);
-      const uint32_t kf = order_key(f, m, a.ordering), kr = order_key(rc, m, a.ordering);
-      s_buf[0][j] = kf < kr ? kf : kr;
+      uint32_t f = (uint32_t)(v >> (64 - 2 * m));
+      uint32_t rc = (uint32_t)(rev_pairs(~v & (~0ull << (64 - 2 * m))) & mmask);
+      uint32_t c[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i > 0) {  // the block's bases j0 .. j0+7+m-1 (<= 22) all sit in v
+          const uint32_t nb = (uint32_t)(v >> (62 - 2 * (i + m - 1))) & 3u;
+          f = ((f << 2) | nb) & mmask;
+          rc = (rc >> 2) | ((3u - nb) << (2 * m - 2));
+        }
+        const uint32_t kf = order_key(f, m, a.ordering), kr = order_key(rc, m, a.ordering);
+        c[i] = kf < kr ? kf : kr;
+      }
+      uint32_t pre = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pre = min(pre, c[i]);
+        if (w < 16) s_key[j0 + i] = c[i];
+        s_pre[j0 + i] = pre;
+      }
+      uint32_t suf = 0xffffffffu;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        suf = min(suf, c[i]);
+        s_suf[j0 + i] = suf;
+      }
+      s_blk[b] = suf;
     }
     __syncthreads();
     // X = N | RS shifted down by one position
     for (uint32_t i = tid; i < (uint32_t)kBitWords - 1; i += kThreads)
       s_x[i] = s_n[i] | (s_rs[i] >> 1) | (s_rs[i + 1] << 31);
-    // 3. sliding minimum by doubling: after the loop M_s[i] = min c[i, i+s)
-    uint32_t len = n_keys, s = 1, cur = 0;
-    while (2 * s <= w) {
-      const uint32_t nl = len - s;
-      const uint32_t* src = s_buf[cur];
-      uint32_t* dst = s_buf[cur ^ 1];
-      for (uint32_t i = tid; i < nl; i += kThreads) {
-        const uint32_t x = src[i], y = src[i + s];
-        dst[i] = x < y ? x : y;
-      }
-      __syncthreads();
-      cur ^= 1;
-      len = nl;
-      s <<= 1;
-    }
-    // 4. μ_p = min(M_s[p], M_s[p+w-s]) and validity (strided positions → ballots)
-    const uint32_t* src = s_buf[cur];
-    uint32_t* mu = s_buf[cur ^ 1];
-    const uint64_t end_p = a.n_bases >= k ? a.n_bases - k + 1 : 0;  // windows start below this
+    __syncthreads();
+    // 3. minimizers and validity of windows 8t .. 8t+7
+    uint32_t mu[kPer];
+    uint32_t vmask = 0;
+    {
+      const uint32_t s0 = tid * kPer;
+      if (w >= 16) {
+        // windows [s, s+w-1] span key blocks t .. be, be >= t+2
+        const uint32_t be0 = (s0 + w - 1) >> 3;
+        uint32_t mid = 0xffffffffu;  // blocks t+1 .. be0-1
+        for (uint32_t b = tid + 1; b < be0; ++b) mid = min(mid, s_blk[b]);
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const uint32_t p = i * kThreads + tid;
-      const uint32_t x = src[p], y = src[p + w - s];
-      mu[p] = x < y ? x : y;
-      const bool valid = p0 + p < end_p && next_set(s_x, p, p + k - 1) == p + k - 1 && !bget(s_n, p + k - 1);
-      const uint32_t bal = __ballot_sync(0xffffffffu, valid);
-      if (lane == 0) s_valid[(i * kThreads + warp * 32) >> 5] = bal;
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t s = s0 + i, e = s + w - 1;
+          const uint32_t m2 = ((e >> 3) > be0) ? min(mid, s_blk[be0]) : mid;
+          mu[i] = min(min(s_suf[s], s_pre[e]), m2);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          uint32_t x = 0xffffffffu;
+          for (uint32_t j = s0 + i; j < s0 + i + w; ++j) x = min(x, s_key[j]);
+          mu[i] = x;
+        }
+      }
+      // window s0+i is valid iff the next X position >= s0+i lies beyond s0+i+k-2
+      // and base s0+i+k-1 is not N. x8 = X bits of the thread's own 8 positions
+      // (s0 is 8-aligned), ns2 = next X at or after s0+8, n8 = N bits of the
+      // 8 window ends.
+      const uint32_t lim = s0 + k - 1 + kPer;
+      const uint32_t x8 = (s_x[s0 >> 5] >> (s0 & 31)) & 0xffu;
+      const uint32_t ns2 = next_set(s_x, s0 + kPer, lim);
+      const uint32_t q = s0 + k - 1, qs = q & 31;
+      uint32_t n8 = s_n[q >> 5] >> qs;
+      if (qs > 24) n8 |= s_n[(q >> 5) + 1] << (32 - qs);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const uint32_t xi = x8 >> i;
+        const uint32_t nxt = xi ? s0 + i + __ffs(xi) - 1 : ns2;
+        const bool valid = p0 + s0 + i < end_p && nxt >= s0 + i + k - 1 && !((n8 >> i) & 1u);
+        vmask |= (uint32_t)valid << i;
+      }
+      s_last[tid] = (vmask >> (kPer - 1)) & 1u ? mu[kPer - 1] : 0xffffffffu;
     }
     __syncthreads();
-    // 5. starts: valid and (tile start, or previous invalid, or μ changed); breaks = !valid | start
-    uint32_t nst = 0;
+    // 4. starts and breaks
+    uint32_t smask = 0;
+    {
+      uint32_t prev = tid ? s_last[tid - 1] : 0xffffffffu;  // ~0: invalid or tile start
+      bool pv = prev != 0xffffffffu;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const uint32_t p = i * kThreads + tid;
-      const bool v = bget(s_valid, p);
-      const bool st = v && (p == 0 || !bget(s_valid, p - 1) || mu[p] != mu[p - 1]);
-      const uint32_t bal = __ballot_sync(0xffffffffu, !v || st);
-      if (lane == 0) s_brk[(i * kThreads + warp * 32) >> 5] = bal;
-      nst += st;
+      for (int i = 0; i < kPer; ++i) {
+        const bool v = (vmask >> i) & 1u;
+        const bool st = v && (!pv || mu[i] != prev);
+        smask |= (uint32_t)st << i;
+        pv = v;
+        prev = mu[i];
+      }
+      // break = !valid | start; 4 threads (32 positions) per bitmap word
+      uint32_t bw = ((~vmask | smask) & 0xffu) << (8 * (tid & 3));
+      bw |= __shfl_xor_sync(0xffffffffu, bw, 1);
+      bw |= __shfl_xor_sync(0xffffffffu, bw, 2);
+      if ((tid & 3) == 0) s_brk[tid >> 2] = bw;
+      if (tid == 0) s_brk[kTile / 32] = 1u;  // tile end
     }
-    if (tid == 0) s_brk[kTile / 32] = 1u;  // tile end
+    const uint32_t nst = __popc(smask);
     const uint32_t incl = warp_incl_scan(nst);
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
@@ -205,14 +265,16 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
     }
     __syncthreads();
     uint64_t idx = s_base + s_warp[warp] + (incl - nst);
-    // 6. emit descriptors and histogram
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const uint32_t p = i * kThreads + tid;
-      if (!bget(s_brk, p) || !bget(s_valid, p)) continue;  // not a start
-      const uint32_t e = next_set(s_brk, p + 1, kTile);
+    // 5. emit descriptors and histogram
+    const uint32_t local_brk = (~vmask | smask) & 0xffu;
+    while (smask) {
+      const int i = __ffs(smask) - 1;
+      smask &= smask - 1;
+      const uint32_t p = tid * kPer + i;
+      const uint32_t later = local_brk & (~0u << (i + 1));
+      const uint32_t e = later ? tid * kPer + __ffs(later) - 1 : next_set(s_brk, tid * kPer + kPer, kTile);
       const uint32_t nwin = e - p;
-      const uint32_t key = mu[p];
+      const uint32_t key = mu[i];
       const uint32_t b = (uint32_t)(((uint64_t)fmix32(key) * B) >> 32);
       if (idx < a.cap) {
         a.desc[idx] = ((p0 + p) << kNwinBits) | (nwin - 1);
@@ -258,7 +320,9 @@ cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms
     tile_reads_kernel<<<(unsigned)g, 256, 0, st>>>(a.read_start, a.n_reads, n_tiles, tile_first);
   }
   const int nh = a.bin_words ? 3 : 2;
-  const int hist_smem = (size_t)nh * a.n_bins * 4 <= 96 * 1024;
+  // per-CTA smem histograms only while small: a large one would cap occupancy,
+  // and spread global REDs are cheap next to this kernel's arithmetic
+  const int hist_smem = a.n_bins <= 2048;
   const size_t dyn = hist_smem ? (size_t)nh * a.n_bins * sizeof(uint32_t) : 0;
   cudaError_t e = cudaFuncSetAttribute(supermer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
