@@ -91,7 +91,7 @@ typedef struct {
   uint32_t max_probes;     /* θ in buckets; 0 = 32 */
   double distinct_ratio;   /* initial ρ̂ = distinct/total estimate; 0 = 0.5 */
   double target_load;      /* α: table load factor target; 0 = 0.7 */
-  uint64_t wave_table_bytes; /* per-wave table budget (kept L2-resident); 0 = 64 MiB */
+  uint64_t wave_table_bytes; /* per-wave table budget (kept L2-resident); 0 = 128 MiB */
   void* stream;            /* cudaStream_t to launch on; NULL = library-owned stream */
   int32_t timing;          /* 1 = record per-kernel CUDA-event times into gerbil_stats */
 } gerbil_config;

@@ -10,7 +10,7 @@
 //   (d)+(e) per wave: count kernel, compaction kernel          (count.cu, compact.cu)
 //   emergency pass for overflowed k-mers; Σ-count invariant check.
 // Table waves reuse one table buffer sized to stay L2-resident
-// (cfg.wave_table_bytes, default 64 MiB of the 126 MB L2), so the hash-table
+// (cfg.wave_table_bytes, default 128 MiB ≈ the 126 MB L2), so the hash-table
 // atomics are served by L2 and HBM sees the streaming traffic only.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -677,7 +677,7 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
   if (cfg.target_load <= 0) cfg.target_load = 0.7;
   if (cfg.target_load > 4.0) return GERBIL_E_USAGE;
   if (cfg.distinct_ratio < 0 || cfg.distinct_ratio > 1) return GERBIL_E_USAGE;
-  if (cfg.wave_table_bytes == 0) cfg.wave_table_bytes = 64ull << 20;
+  if (cfg.wave_table_bytes == 0) cfg.wave_table_bytes = 128ull << 20;
   gerbil_ctx* ctx = new gerbil_ctx();
   ctx->cfg = cfg;
   ctx->rho = cfg.distinct_ratio > 0 ? cfg.distinct_ratio : 0.5;

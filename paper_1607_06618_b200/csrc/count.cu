@@ -19,6 +19,8 @@
 #include "table_inline.cuh"
 #include "count_inline.cuh"
 
+#include <stdlib.h>
+
 namespace gerbil {
 namespace {
 
@@ -274,9 +276,8 @@ cudaError_t launch_count_keys_w(const CountKeysArgs& a, int sms, cudaStream_t st
     return cudaErrorInvalidValue;                                     \
   } while (0)
 
-template <int W, bool TWO>
-cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
-  constexpr int U = 2;
+template <int W, bool TWO, int U>
+cudaError_t launch_inline_u(const CountArgs& a, int sms, cudaStream_t st) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_inline_kernel<W, TWO, U>, 128, 0);
   if (per_sm < 1) per_sm = 1;
@@ -287,6 +288,26 @@ cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
   if (grid == 0) return cudaSuccess;
   count_inline_kernel<W, TWO, U><<<(unsigned)grid, 128, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+// windows in flight per lane (tuning knob; GERBIL_COUNT_U overrides). U=1 won
+// the B200 sweep (profiles/r01_sweep.txt): fewer registers → more resident warps.
+int count_u() {
+  static int u = [] {
+    const char* e = getenv("GERBIL_COUNT_U");
+    const int v = e ? atoi(e) : 1;
+    return (v == 1 || v == 2 || v == 4) ? v : 1;
+  }();
+  return u;
+}
+
+template <int W, bool TWO>
+cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
+  switch (count_u()) {
+    case 1: return launch_inline_u<W, TWO, 1>(a, sms, st);
+    case 4: return launch_inline_u<W, TWO, 4>(a, sms, st);
+  }
+  return launch_inline_u<W, TWO, 2>(a, sms, st);
 }
 
 template <int W, bool TWO>
