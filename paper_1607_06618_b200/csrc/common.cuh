@@ -85,11 +85,17 @@ __device__ __forceinline__ bool key_less(const uint64_t (&a)[W], const uint64_t 
   return false;
 }
 
+// Table hash of a canonical key: multiply-xorshift over the words (one 64-bit
+// multiply per word plus one finaliser). Only its distribution matters — it is
+// not observable in the output (reading Q11).
 template <int W>
 __device__ __forceinline__ uint64_t key_hash(const uint64_t (&c)[W]) {
-  uint64_t h = fmix64(c[0] ^ 0x2545F4914F6CDD1Dull);
+  uint64_t h = c[0] * 0x9E3779B97F4A7C15ull;
 #pragma unroll
-  for (int i = 1; i < W; ++i) h = fmix64(h ^ c[i]);
+  for (int i = 1; i < W; ++i) h = (h ^ (h >> 29)) + c[i] * 0xC2B2AE3D27D4EB4Full;
+  h ^= h >> 32;
+  h *= 0xD6E8FEB86659FD93ull;
+  h ^= h >> 32;
   return h;
 }
 

@@ -276,38 +276,20 @@ cudaError_t launch_count_keys_w(const CountKeysArgs& a, int sms, cudaStream_t st
     return cudaErrorInvalidValue;                                     \
   } while (0)
 
-template <int W, bool TWO, int U>
-cudaError_t launch_inline_u(const CountArgs& a, int sms, cudaStream_t st) {
+// One window per lane per step (the B200 sweep in profiles/r01_sweep.txt: more
+// resident warps beat more windows per lane).
+template <int W, bool TWO>
+cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_inline_kernel<W, TWO, U>, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_inline_kernel<W, TWO>, 128, 0);
   if (per_sm < 1) per_sm = 1;
   const uint64_t chunks = (a.d1 - a.d0 + 31) / 32;
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (chunks + 3) / 4;
   if (grid > need) grid = need;
   if (grid == 0) return cudaSuccess;
-  count_inline_kernel<W, TWO, U><<<(unsigned)grid, 128, 0, st>>>(a);
+  count_inline_kernel<W, TWO><<<(unsigned)grid, 128, 0, st>>>(a);
   return cudaGetLastError();
-}
-
-// windows in flight per lane (tuning knob; GERBIL_COUNT_U overrides). U=1 won
-// the B200 sweep (profiles/r01_sweep.txt): fewer registers → more resident warps.
-int count_u() {
-  static int u = [] {
-    const char* e = getenv("GERBIL_COUNT_U");
-    const int v = e ? atoi(e) : 1;
-    return (v == 1 || v == 2 || v == 4) ? v : 1;
-  }();
-  return u;
-}
-
-template <int W, bool TWO>
-cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
-  switch (count_u()) {
-    case 1: return launch_inline_u<W, TWO, 1>(a, sms, st);
-    case 4: return launch_inline_u<W, TWO, 4>(a, sms, st);
-  }
-  return launch_inline_u<W, TWO, 2>(a, sms, st);
 }
 
 template <int W, bool TWO>

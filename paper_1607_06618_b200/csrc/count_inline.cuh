@@ -7,13 +7,15 @@
 //    shared-memory stage, and the NEXT chunk's words are prefetched into
 //    registers while the current chunk is counted, so no DRAM latency sits on
 //    the per-window chain;
-//  - lanes walk the chunk's windows 32·U at a time, extract each k-mer from
-//    smem, canonicalise, hash;
-//  - probing runs in batched rounds: every pending window examines one bucket
-//    (both 32-byte sectors prefetched), REDs are fired, CASes are issued for
-//    all windows before any result is consumed; windows whose bucket is full
-//    move to the next bucket in the next round (θ buckets, then the emergency
-//    area).
+//  - lanes walk the chunk's windows 32 at a time, extract each k-mer from
+//    smem, canonicalise, hash, load the bucket (two 32-byte
+//    sectors) and resolve it in ONE probe: a matching k-mer → RED on its
+//    count; an empty slot → one 128-bit CAS claim;
+//  - the few windows that do not resolve there (bucket full → next trial, lost
+//    CAS race, half-visible slot) are pushed to a per-warp retry queue in
+//    shared memory and drained 32 at a time, so a rare second probe never
+//    costs a whole warp-round; after θ buckets a k-mer goes to the emergency
+//    area.
 #pragma once
 #include "common.cuh"
 #include "kernels.h"
@@ -22,6 +24,7 @@
 namespace gerbil {
 
 constexpr int kStageWords = 8;  // packed words staged per super-mer (≤ 256 bases)
+constexpr int kQueue = 64;      // per-warp retry queue entries
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
 #pragma unroll
@@ -45,13 +48,102 @@ __device__ __forceinline__ void extract_smem(const uint64_t* s, uint32_t o, uint
   if (tail < 64) x[W - 1] &= ~0ull << (64 - tail);
 }
 
-template <int W, bool TWO, int U>
+struct RetryQueue {
+  uint64_t k0[kQueue], k1[kQueue], bkt[kQueue];
+  uint32_t probes[kQueue];
+};
+
+// One probe of bucket b for key (k0, k1). Returns 0 = resolved, 1 = retry the
+// same bucket (lost race / half-visible slot), 2 = bucket full (next trial).
+template <bool TWO>
+__device__ __forceinline__ int probe_once(unsigned char* table, uint64_t b, uint64_t k0, uint64_t k1,
+                                          const uint64_t (&w)[8]) {
+  uint64_t* bk = reinterpret_cast<uint64_t*>(table + b * kInlineBucketBytes);
+  int ms = -1, es = -1;
+  bool torn = false;
+#pragma unroll
+  for (int s = 3; s >= 0; --s) {
+    if (inline_match(w[2 * s], w[2 * s + 1], k0, k1)) ms = s;
+    if (w[2 * s] == 0ull) es = s;
+    if (TWO) torn |= (w[2 * s] != 0ull) && !(w[2 * s + 1] >> 63);
+  }
+  if (ms >= 0) {  // matching k-mer → count + 1
+    atomicAdd(inline_count(bk + 2 * ms), 1u);
+    return 0;
+  }
+  if (torn) return 1;  // a slot was read mid-claim: look again
+  if (es < 0) return 2;
+  const Slot16 old = cas128(bk + 2 * es, 0ull, 0ull, k0, k1 | 1ull);  // empty entry → (x, 1)
+  if (old.w0 == 0ull) return 0;
+  if (inline_match(old.w0, old.w1, k0, k1)) {
+    atomicAdd(inline_count(bk + 2 * es), 1u);
+    return 0;
+  }
+  return 1;  // lost the slot to another k-mer: re-examine this bucket
+}
+
+template <int W, bool TWO>
 __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
   __shared__ uint64_t s_stage[4][32 * kStageWords];
+  __shared__ RetryQueue s_q[4];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   uint64_t* stage = s_stage[wib];
+  RetryQueue& q = s_q[wib];
+  uint32_t qn = 0;  // warp-uniform queue length
   const uint64_t n_chunks = (a.d1 - a.d0 + 31) / 32;
   uint32_t first = 0, more = 0, maxp = 0;
+
+  // push the lanes in `mask` (each with its own entry) to the retry queue
+  auto push = [&](uint32_t mask, uint64_t k0, uint64_t k1, uint64_t b, uint32_t p) {
+    if ((mask >> lane) & 1u) {
+      const uint32_t i = qn + __popc(mask & ((1u << lane) - 1u));
+      q.k0[i] = k0;
+      q.k1[i] = k1;
+      q.bkt[i] = b;
+      q.probes[i] = p;
+    }
+    qn += __popc(mask);
+  };
+  // resolve one probe for the lanes in `act`; returns the lanes to requeue
+  auto settle_lanes = [&](bool act, uint64_t k0, uint64_t k1, uint64_t& b, uint32_t& p,
+                          const uint64_t (&w)[8]) -> bool {
+    bool again = false;
+    if (act) {
+      const int r = probe_once<TWO>(a.t.table, b, k0, k1, w);
+      if (r == 0) {
+        if (p == 1) ++first;
+        else { ++more; maxp = max(maxp, p); }
+      } else if (r == 2 && p >= a.t.max_probes) {  // θ trials exhausted → emergency
+        uint64_t ch[2] = {k0, k1}, key[2];
+        from_chunks(ch, TWO ? 2u : 1u, key, (uint32_t)W);
+        const unsigned long long e = atomicAdd(a.t.ovf_n, 1ull);
+        if (e < a.t.ovf_cap) {
+#pragma unroll
+          for (int v = 0; v < W; ++v) a.t.ovf[e * W + v] = key[v];
+        }
+      } else {
+        if (r == 2) {  // bucket occupied by other k-mers → next trial
+          b = (b + 1 == a.t.nb) ? 0 : b + 1;
+          ++p;
+        }
+        again = true;
+      }
+    }
+    return again;
+  };
+  // drain 32 queued windows (one per lane), requeueing the unresolved
+  auto drain = [&]() {
+    const uint32_t base = qn - 32;
+    uint64_t k0 = q.k0[base + lane], k1 = q.k1[base + lane], b = q.bkt[base + lane];
+    uint32_t p = q.probes[base + lane];
+    __syncwarp();
+    qn = base;
+    uint64_t w[8];
+    ld_bucket_inline(reinterpret_cast<const uint64_t*>(a.t.table + b * kInlineBucketBytes), w);
+    const bool again = settle_lanes(true, k0, k1, b, p, w);
+    push(__ballot_sync(0xffffffffu, again), k0, k1, b, p);
+    __syncwarp();
+  };
 
   // prefetch state of the next chunk (registers)
   unsigned long long nxt = 0;
@@ -70,7 +162,7 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
       const uint32_t nwords = ((uint32_t)(n_pos & 31) + n_nw + a.k - 1 + 31) >> 5;
       const uint64_t* src = a.codes + (n_pos >> 5);
 #pragma unroll
-      for (int q = 0; q < kStageWords; ++q) n_words[q] = (q < (int)nwords) ? __ldg(src + q) : 0ull;
+      for (int s = 0; s < kStageWords; ++s) n_words[s] = (s < (int)nwords) ? __ldg(src + s) : 0ull;
     }
   };
   if (lane == 0) nxt = atomicAdd(a.work, 1ull);
@@ -85,7 +177,7 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
     const uint32_t nw = n_nw;
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < kStageWords; ++q) stage[lane * kStageWords + q] = n_words[q];
+    for (int s = 0; s < kStageWords; ++s) stage[lane * kStageWords + s] = n_words[s];
     const bool staged = ((uint32_t)(pos & 31) + nw + a.k - 1) <= 32u * kStageWords;
     if (lane == 0) nxt = atomicAdd(a.work, 1ull);
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
@@ -95,113 +187,59 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
     const uint32_t incl = warp_incl_scan_u32(nw), excl = incl - nw;
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t stage_mask = __ballot_sync(0xffffffffu, staged);
-    for (uint32_t base = 0; base < total; base += 32 * U) {
-      uint64_t k0[U], k1[U], bkt[U], w[U][8];
-      uint64_t ckey[U][W];
-      bool pend[U];
-      uint32_t probes[U];
+    for (uint32_t base = 0; base < total; base += 32) {
+      const uint32_t i = base + lane;
+      int j = 0;  // super-mer (lane) holding window i: #lanes with incl <= i
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = base + u * 32 + lane;
-        int j = 0;  // super-mer (lane) holding window i: #lanes with incl <= i
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
-          if (v <= i) j += step;
-        }
-        const uint64_t pj = __shfl_sync(0xffffffffu, pos, j);
-        const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
-        pend[u] = i < total;
-        probes[u] = pend[u] ? 1u : 0xffffffffu;
-        uint64_t x[W], r[W];
-        if ((stage_mask >> j) & 1u) {
-          extract_smem<W>(stage + j * kStageWords, (uint32_t)(pj & 31) + (i - ej), a.k, x);
-        } else {
-          extract_kmer<W>(a.codes, pend[u] ? pj + (i - ej) : 0ull, a.k, x);
-        }
-        reverse_complement<W>(x, a.k, r);
-        const bool use_r = key_less<W>(r, x);
-#pragma unroll
-        for (int v = 0; v < W; ++v) ckey[u][v] = use_r ? r[v] : x[v];
-        uint64_t ch[2];
-        to_chunks<W, 2>(ckey[u], ch);
-        k0[u] = ch[0];
-        k1[u] = TWO ? ch[1] : 0ull;
-        bkt[u] = bucket_of(key_hash<W>(ckey[u]), a.t.nb);
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+        if (v <= i) j += step;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (pend[u]) ld_bucket_inline(reinterpret_cast<const uint64_t*>(a.t.table + bkt[u] * kInlineBucketBytes), w[u]);
-      // batched probe rounds (Alg. 1 trials)
-      for (;;) {
-        bool anyp = false;
-#pragma unroll
-        for (int u = 0; u < U; ++u) anyp |= pend[u];
-        if (!__any_sync(0xffffffffu, anyp)) break;
-        int cas_slot[U];
-        Slot16 old[U];
-        bool reload[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          cas_slot[u] = -1;
-          reload[u] = false;
-          if (!pend[u]) continue;
-          uint64_t* bk = reinterpret_cast<uint64_t*>(a.t.table + bkt[u] * kInlineBucketBytes);
-#pragma unroll
-          for (int s = 0; s < 4; ++s) settle<TWO>(bk + 2 * s, w[u][2 * s], w[u][2 * s + 1]);
-          int ms = -1, es = -1;
-#pragma unroll
-          for (int s = 3; s >= 0; --s) {
-            if (inline_match(w[u][2 * s], w[u][2 * s + 1], k0[u], k1[u])) ms = s;
-            if (w[u][2 * s] == 0ull) es = s;
-          }
-          if (ms >= 0) {  // matching k-mer → count + 1
-            atomicAdd(inline_count(bk + 2 * ms), 1u);
-            pend[u] = false;
-          } else if (es >= 0) {  // empty entry → claim (x, 1)
-            cas_slot[u] = es;
-            old[u] = cas128(bk + 2 * es, 0ull, 0ull, k0[u], k1[u] | 1ull);
-          } else if (probes[u] >= a.t.max_probes) {  // θ trials exhausted → emergency
-            const unsigned long long e = atomicAdd(a.t.ovf_n, 1ull);
-            if (e < a.t.ovf_cap) {
-#pragma unroll
-              for (int v = 0; v < W; ++v) a.t.ovf[e * W + v] = ckey[u][v];
-            }
-            pend[u] = false;
-            probes[u] = 0;
-          } else {  // bucket occupied by other k-mers → next trial
-            bkt[u] = (bkt[u] + 1 == a.t.nb) ? 0 : bkt[u] + 1;
-            ++probes[u];
-            reload[u] = true;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (cas_slot[u] < 0) continue;
-          if (old[u].w0 == 0ull) {
-            pend[u] = false;
-          } else if (inline_match(old[u].w0, old[u].w1, k0[u], k1[u])) {
-            uint64_t* bk = reinterpret_cast<uint64_t*>(a.t.table + bkt[u] * kInlineBucketBytes);
-            atomicAdd(inline_count(bk + 2 * cas_slot[u]), 1u);
-            pend[u] = false;
-          } else {
-            reload[u] = true;  // lost the slot to another k-mer: re-examine this bucket
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (reload[u])
-            ld_bucket_inline(reinterpret_cast<const uint64_t*>(a.t.table + bkt[u] * kInlineBucketBytes), w[u]);
-          if (!pend[u] && !reload[u] && probes[u] != 0xffffffffu) {
-            // resolved this round: record probe statistics once
-            const uint32_t p = probes[u];
-            if (p == 1) ++first;
-            else if (p > 1) { ++more; maxp = max(maxp, p); }
-            probes[u] = 0xffffffffu;
-          }
-        }
+      const uint64_t pj = __shfl_sync(0xffffffffu, pos, j);
+      const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
+      const bool act = i < total;
+      uint64_t x[W], r[W], c[W];
+      if ((stage_mask >> j) & 1u) {
+        extract_smem<W>(stage + j * kStageWords, (uint32_t)(pj & 31) + (i - ej), a.k, x);
+      } else {
+        extract_kmer<W>(a.codes, act ? pj + (i - ej) : 0ull, a.k, x);
       }
+      reverse_complement<W>(x, a.k, r);
+      const bool use_r = key_less<W>(r, x);
+#pragma unroll
+      for (int v = 0; v < W; ++v) c[v] = use_r ? r[v] : x[v];
+      uint64_t ch[2];
+      to_chunks<W, 2>(c, ch);
+      const uint64_t k0 = ch[0], k1 = TWO ? ch[1] : 0ull;
+      uint64_t b = bucket_of(key_hash<W>(c), a.t.nb);
+      uint32_t p = 1;
+      uint64_t w[8];
+      if (act) ld_bucket_inline(reinterpret_cast<const uint64_t*>(a.t.table + b * kInlineBucketBytes), w);
+      const bool again = settle_lanes(act, k0, k1, b, p, w);
+      push(__ballot_sync(0xffffffffu, again), k0, k1, b, p);
+      __syncwarp();
+      while (qn >= 32) drain();
     }
+  }
+  // finish the queue: full batches first, then the remainder (lanes >= qn idle)
+  while (qn >= 32) drain();
+  while (qn > 0) {
+    const bool mine = lane < qn;
+    uint64_t k0 = 0, k1 = 0, b = 0;
+    uint32_t p = 0;
+    if (mine) {
+      k0 = q.k0[lane];
+      k1 = q.k1[lane];
+      b = q.bkt[lane];
+      p = q.probes[lane];
+    }
+    __syncwarp();
+    qn = 0;
+    uint64_t w[8];
+    if (mine) ld_bucket_inline(reinterpret_cast<const uint64_t*>(a.t.table + b * kInlineBucketBytes), w);
+    const bool again = settle_lanes(mine, k0, k1, b, p, w);
+    push(__ballot_sync(0xffffffffu, again), k0, k1, b, p);
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

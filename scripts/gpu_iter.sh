@@ -3,7 +3,7 @@
 set -u
 mkdir -p gpurun_out
 python build_native.py > gpurun_out/build.log 2>&1
-timeout 300 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/summary.txt
+timeout 300 python -m pytest tests -x -q -m "gpu and not slow" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/summary.txt
 tail -2 gpurun_out/pytest_gpu.log >> gpurun_out/summary.txt
 timeout 240 python bench.py --reads 5000000 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_small.log 2>&1; echo "bench_small rc=$?" >> gpurun_out/summary.txt
 if [ "${FULL:-1}" = "1" ]; then

@@ -21,19 +21,26 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 C1 = synth.Workload(seed=2, genome_len=240_000_000, read_len=100, n_reads=50_000_000, err=0.0033, nrate=0.0001)
 K, M, SAMPLE = 40, 7, 4096
-LETTERS = np.frombuffer(b"ACGT", dtype=np.uint8).astype(np.uint64)
-FNV_OFF, FNV_PRIME = np.uint64(1469598103934665603), np.uint64(1099511628211)
 
 
 def _fnv_keep(keys: np.ndarray, k: int, mod: int) -> np.ndarray:
-    """FNV-1a-64 over the ASCII decoding of each key (harness-side), == 0 mod `mod`."""
-    h = np.full(keys.shape[0], FNV_OFF, dtype=np.uint64)
-    with np.errstate(over="ignore"):
+    """FNV-1a-64 over the ASCII decoding of each key (harness-side, on the GPU
+    with torch int64 arithmetic = wrap-around mod 2^64), == 0 mod `mod` (a power of 2)."""
+    import torch
+
+    out = np.zeros(keys.shape[0], dtype=bool)
+    letters = torch.tensor([65, 67, 71, 84], dtype=torch.int64, device="cuda")
+    prime = torch.tensor(1099511628211, dtype=torch.int64, device="cuda")
+    off = np.uint64(1469598103934665603).astype(np.int64)
+    step = 50_000_000
+    for a in range(0, keys.shape[0], step):
+        kk = torch.from_numpy(keys[a:a + step].view(np.int64)).cuda()
+        h = torch.full((kk.shape[0],), int(off), dtype=torch.int64, device="cuda")
         for i in range(k):
-            code = (keys[:, i // 32] >> np.uint64(62 - 2 * (i % 32))) & np.uint64(3)
-            h ^= LETTERS[code.astype(np.int64)]
-            h *= FNV_PRIME
-    return (h % np.uint64(mod)) == 0
+            code = (kk[:, i // 32] >> (62 - 2 * (i % 32))) & 3  # arithmetic shift; masked to 2 bits
+            h = (h ^ letters[code]) * prime
+        out[a:a + step] = ((h & (mod - 1)) == 0).cpu().numpy()
+    return out
 
 
 def test_c1_fullsize_sampled_parity():
@@ -52,10 +59,7 @@ def test_c1_fullsize_sampled_parity():
         keys, counts = g.fetch(sorted=False)
     del codes, nmask, rs
     assert st["count_sum"] == st["valid_windows"]
-    keep = np.zeros(keys.shape[0], dtype=bool)
-    step = 20_000_000
-    for a in range(0, keys.shape[0], step):
-        keep[a:a + step] = _fnv_keep(keys[a:a + step], K, SAMPLE)
+    keep = _fnv_keep(keys, K, SAMPLE)
     sk, sc = keys[keep], counts[keep]
     del keys, counts
     order = np.lexsort(tuple(sk[:, j] for j in reversed(range(sk.shape[1]))))
