@@ -9,7 +9,7 @@
 // (PAPER.md:426).
 //
 // B200 design: the read batch is one packed base
-// stream; a persistent CTA takes tiles of kTile = 2048 window start positions,
+// stream; a persistent CTA takes tiles of kSTile = 1024 window start positions,
 // independent of read length (100-bp and 10-kbp reads balance the same way).
 //   0. tile_reads_kernel: first read of every tile (one pass over read_start);
 //   1. stage the tile's packed codes, N-mask and read starts in smem
@@ -36,14 +36,17 @@
 namespace gerbil {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
+constexpr uint32_t kSTile = 1024;  // window positions per tile (also caps super-mer length)
 constexpr int kWarps = kThreads / 32;
-constexpr int kPer = kTile / kThreads;  // 8 window positions per thread
+constexpr int kPer = kSTile / kThreads;  // 8 window positions per thread
 constexpr int kMaxK = 200;
-constexpr int kCodeWords = (kTile + kMaxK + 31) / 32 + 2;        // u64 words of 32 bases
-constexpr int kBitWords = ((kTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
-constexpr int kKeyLen = kTile + kMaxK;                           // >= kTile + k - m
-constexpr int kKeyBlocks = (kKeyLen + 7) / 8;
+constexpr int kKB = 10;                     // keys per key block (one block per thread)
+constexpr int kKeyLen = kThreads * kKB;     // 1280 >= kSTile + k - m for every k <= 200
+constexpr int kKeyBlocks = kThreads;
+constexpr int kCodeWords = (kKeyLen + 16 + 31) / 32 + 2;          // u64 words of 32 bases
+constexpr int kBitWords = ((kSTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
+static_assert(kKeyLen >= (int)kSTile + kMaxK - 1, "key blocks must cover every window");
 
 __device__ __forceinline__ bool bget(const uint32_t* bm, uint32_t i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
 
@@ -54,6 +57,18 @@ __device__ __forceinline__ uint32_t next_set(const uint32_t* bm, uint32_t from, 
   while (!v) {
     if (((++w) << 5) >= limit) return limit;
     v = bm[w];
+  }
+  const uint32_t i = (w << 5) + __ffs(v) - 1;
+  return i < limit ? i : limit;
+}
+
+// smallest position q in [from, limit) with X(q) = N(q) | RS(q+1) set, or limit
+__device__ __forceinline__ uint32_t next_x(const uint32_t* n, const uint32_t* rs, uint32_t from, uint32_t limit) {
+  uint32_t w = from >> 5;
+  uint32_t v = (n[w] | (rs[w] >> 1) | (rs[w + 1] << 31)) & (~0u << (from & 31));
+  while (!v) {
+    if (((++w) << 5) >= limit) return limit;
+    v = n[w] | (rs[w] >> 1) | (rs[w + 1] << 31);
   }
   const uint32_t i = (w << 5) + __ffs(v) - 1;
   return i < limit ? i : limit;
@@ -79,33 +94,31 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
-__device__ __forceinline__ uint32_t base_at(const uint64_t* codes, uint32_t j) {
-  return (uint32_t)(codes[j >> 5] >> (62 - 2 * (j & 31))) & 3u;
-}
-
 __global__ void tile_reads_kernel(const uint64_t* __restrict__ read_start, uint64_t n_reads,
                                   uint64_t n_tiles, uint64_t* __restrict__ tile_first) {
-  // tile t starts at p0 = t*kTile; its first read is the last r with read_start[r] <= p0
+  // tile t starts at p0 = t*kSTile; its first read is the last r with read_start[r] <= p0
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n_reads;
        r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t a = read_start[r], b = read_start[r + 1];
     if (a == b) continue;  // empty read owns no position
-    for (uint64_t t = (a + kTile - 1) / kTile; t * kTile < b && t < n_tiles; ++t) tile_first[t] = r;
+    for (uint64_t t = (a + kSTile - 1) / kSTile; t * kSTile < b && t < n_tiles; ++t) tile_first[t] = r;
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 5)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_t n_tiles, int hist_smem) {
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
   __shared__ uint32_t s_rs[kBitWords];   // read-start bits
-  __shared__ uint32_t s_x[kBitWords];    // N(q) | RS(q+1)
   __shared__ uint32_t s_key[kKeyLen];    // c_j
   __shared__ uint32_t s_pre[kKeyLen];    // min over c[8b .. j] (j in block b)
   __shared__ uint32_t s_suf[kKeyLen];    // min over c[j .. 8b+7]
   __shared__ uint32_t s_blk[kKeyBlocks]; // min over block b
-  __shared__ uint32_t s_brk[kTile / 32 + 1];
+  __shared__ uint32_t s_brk[kSTile / 32 + 1];
   __shared__ uint32_t s_last[kThreads];  // μ of window 8t+7, or ~0 if invalid
+  __shared__ uint16_t s_sp[kSTile];      // the tile's super-mer start positions
+  __shared__ uint32_t s_smu[kSTile];     // and their minimizer keys
+  __shared__ uint32_t s_nst;
   __shared__ uint32_t s_warp[kWarps];
   __shared__ unsigned long long s_base;
   extern __shared__ uint32_t s_hist[];   // [2 or 3][n_bins] when hist_smem
@@ -113,9 +126,8 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint32_t k = a.k, m = a.m, B = a.n_bins;
   const uint32_t w = k - m + 1;
-  const uint32_t n_keys = kTile + k - m;  // m-mers needed by the tile's windows
-  const uint32_t n_blocks = (n_keys + 7) / 8;
-  const uint32_t n_bits = kTile + k;      // staged base positions
+  const uint32_t n_keys = kSTile + k - m;  // m-mers needed by the tile's windows
+  const uint32_t n_bits = kSTile + k;      // staged base positions
   const uint64_t n_code_words = (a.n_bases + 31) / 32, n_mask_words = (a.n_bases + 63) / 64;
   const int nh = a.bin_words ? 3 : 2;
   const uint32_t mmask = (uint32_t)((1ull << (2 * m)) - 1);
@@ -128,7 +140,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
   uint64_t my_windows = 0;
 
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const uint64_t p0 = tile * kTile;
+    const uint64_t p0 = tile * kSTile;
     // 1. stage codes and N bits (u64 MSB-first → u32 LSB-first via bit reversal)
     const uint64_t wb = p0 >> 5;
     for (uint32_t i = tid; i < (uint32_t)kCodeWords; i += kThreads)
@@ -150,18 +162,19 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       if (v >= lim) break;
       if (v > p0) atomicOr(&s_rs[(uint32_t)(v - p0) >> 5], 1u << ((uint32_t)(v - p0) & 31));
     }
-    // 2. rolling strand-symmetric m-mer keys, block prefix/suffix minima
-    for (uint32_t b = tid; b < n_blocks; b += kThreads) {
-      const uint32_t j0 = 8 * b;
+    // 2. rolling strand-symmetric m-mer keys of key block t (kKB keys, exactly
+    //    one block per thread), block prefix/suffix minima
+    {
+      const uint32_t j0 = kKB * tid;
       // initial m-mer at j0
       const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
       const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
       uint32_t f = (uint32_t)(v >> (64 - 2 * m));
       uint32_t rc = (uint32_t)(rev_pairs(~v & (~0ull << (64 - 2 * m))) & mmask);
-      uint32_t c[8];
+      uint32_t c[kKB];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i > 0) {  // the block's bases j0 .. j0+7+m-1 (<= 22) all sit in v
+      for (int i = 0; i < kKB; ++i) {
+        if (i > 0) {  // the block's bases j0 .. j0+kKB-1+m-1 (<= 24) all sit in v
           const uint32_t nb = (uint32_t)(v >> (62 - 2 * (i + m - 1))) & 3u;
           f = ((f << 2) | nb) & mmask;
           rc = (rc >> 2) | ((3u - nb) << (2 * m - 2));
@@ -171,38 +184,39 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       }
       uint32_t pre = 0xffffffffu;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < kKB; ++i) {
         pre = min(pre, c[i]);
-        if (w < 16) s_key[j0 + i] = c[i];
+        if (w < 2 * kKB) s_key[j0 + i] = c[i];
         s_pre[j0 + i] = pre;
       }
       uint32_t suf = 0xffffffffu;
 #pragma unroll
-      for (int i = 7; i >= 0; --i) {
+      for (int i = kKB - 1; i >= 0; --i) {
         suf = min(suf, c[i]);
         s_suf[j0 + i] = suf;
       }
-      s_blk[b] = suf;
+      s_blk[tid] = suf;
     }
-    __syncthreads();
-    // X = N | RS shifted down by one position
-    for (uint32_t i = tid; i < (uint32_t)kBitWords - 1; i += kThreads)
-      s_x[i] = s_n[i] | (s_rs[i] >> 1) | (s_rs[i + 1] << 31);
     __syncthreads();
     // 3. minimizers and validity of windows 8t .. 8t+7
     uint32_t mu[kPer];
     uint32_t vmask = 0;
     {
       const uint32_t s0 = tid * kPer;
-      if (w >= 16) {
-        // windows [s, s+w-1] span key blocks t .. be, be >= t+2
-        const uint32_t be0 = (s0 + w - 1) >> 3;
-        uint32_t mid = 0xffffffffu;  // blocks t+1 .. be0-1
-        for (uint32_t b = tid + 1; b < be0; ++b) mid = min(mid, s_blk[b]);
+      if (w >= 2 * kKB) {
+        // window [s, e] (e = s+w-1) = suffix of block s/kKB, the whole blocks in
+        // between, prefix of block e/kKB. The 8 windows share every whole block
+        // strictly between bsL = (s0+7)/kKB and beF = (s0+w-1)/kKB.
+        const uint32_t bsL = (s0 + kPer - 1) / kKB, beF = (s0 + w - 1) / kKB;
+        uint32_t mid = 0xffffffffu;
+        for (uint32_t b = bsL + 1; b < beF; ++b) mid = min(mid, s_blk[b]);
+        const uint32_t xa = s_blk[bsL], xb = s_blk[beF];
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
           const uint32_t s = s0 + i, e = s + w - 1;
-          const uint32_t m2 = ((e >> 3) > be0) ? min(mid, s_blk[be0]) : mid;
+          uint32_t m2 = mid;
+          if (s / kKB < bsL) m2 = min(m2, xa);
+          if (e / kKB > beF) m2 = min(m2, xb);
           mu[i] = min(min(s_suf[s], s_pre[e]), m2);
         }
       } else {
@@ -218,8 +232,11 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       // (s0 is 8-aligned), ns2 = next X at or after s0+8, n8 = N bits of the
       // 8 window ends.
       const uint32_t lim = s0 + k - 1 + kPer;
-      const uint32_t x8 = (s_x[s0 >> 5] >> (s0 & 31)) & 0xffu;
-      const uint32_t ns2 = next_set(s_x, s0 + kPer, lim);
+      const uint32_t s0w = s0 >> 5, s0b = s0 & 31;  // s0b in {0, 8, 16, 24}
+      uint32_t rs8 = s_rs[s0w] >> (s0b + 1);         // RS bits s0+1 .. s0+8
+      if (s0b == 24) rs8 |= s_rs[s0w + 1] << 7;
+      const uint32_t x8 = ((s_n[s0w] >> s0b) | rs8) & 0xffu;
+      const uint32_t ns2 = next_x(s_n, s_rs, s0 + kPer, lim);
       const uint32_t q = s0 + k - 1, qs = q & 31;
       uint32_t n8 = s_n[q >> 5] >> qs;
       if (qs > 24) n8 |= s_n[(q >> 5) + 1] << (32 - qs);
@@ -251,7 +268,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       bw |= __shfl_xor_sync(0xffffffffu, bw, 1);
       bw |= __shfl_xor_sync(0xffffffffu, bw, 2);
       if ((tid & 3) == 0) s_brk[tid >> 2] = bw;
-      if (tid == 0) s_brk[kTile / 32] = 1u;  // tile end
+      if (tid == 0) s_brk[kSTile / 32] = 1u;  // tile end
     }
     const uint32_t nst = __popc(smask);
     const uint32_t incl = warp_incl_scan(nst);
@@ -261,27 +278,37 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
       const uint32_t v = tid < kWarps ? s_warp[tid] : 0;
       const uint32_t t = warp_incl_scan(v);
       if (tid < kWarps) s_warp[tid] = t - v;  // exclusive
-      if (tid == kWarps - 1) s_base = atomicAdd(a.n_supermers, (unsigned long long)t);
+      if (tid == kWarps - 1) {
+        s_base = atomicAdd(a.n_supermers, (unsigned long long)t);
+        s_nst = t;
+      }
     }
     __syncthreads();
-    uint64_t idx = s_base + s_warp[warp] + (incl - nst);
-    // 5. emit descriptors and histogram
-    const uint32_t local_brk = (~vmask | smask) & 0xffu;
-    while (smask) {
-      const int i = __ffs(smask) - 1;
-      smask &= smask - 1;
-      const uint32_t p = tid * kPer + i;
-      const uint32_t later = local_brk & (~0u << (i + 1));
-      const uint32_t e = later ? tid * kPer + __ffs(later) - 1 : next_set(s_brk, tid * kPer + kPer, kTile);
-      const uint32_t nwin = e - p;
-      const uint32_t key = mu[i];
+    // 5. the tile's starts go to a shared list at their scan offsets, then all
+    //    threads emit them together (full lanes, coalesced descriptor writes)
+    {
+      uint32_t o = s_warp[warp] + (incl - nst);
+      while (smask) {
+        const int i = __ffs(smask) - 1;
+        smask &= smask - 1;
+        s_sp[o] = (uint16_t)(tid * kPer + i);
+        s_smu[o] = mu[i];
+        ++o;
+      }
+    }
+    __syncthreads();
+    const uint32_t n_st_tile = s_nst;
+    for (uint32_t e = tid; e < n_st_tile; e += kThreads) {
+      const uint32_t p = s_sp[e];
+      const uint32_t nwin = next_set(s_brk, p + 1, kSTile) - p;
+      const uint32_t key = s_smu[e];
       const uint32_t b = (uint32_t)(((uint64_t)fmix32(key) * B) >> 32);
+      const uint64_t idx = s_base + e;
       if (idx < a.cap) {
         a.desc[idx] = ((p0 + p) << kNwinBits) | (nwin - 1);
         a.bin[idx] = b;
         if (a.mu) a.mu[idx] = key;
       }
-      ++idx;
       my_windows += nwin;
       if (hist_smem) {
         atomicAdd(&h_win[b], nwin);
@@ -312,7 +339,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
 }  // namespace
 
 cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms, cudaStream_t st) {
-  const uint64_t n_tiles = (a.n_bases + kTile - 1) / kTile;
+  const uint64_t n_tiles = (a.n_bases + kSTile - 1) / kSTile;
   if (n_tiles == 0) return cudaSuccess;
   if (a.n_reads) {
     uint64_t g = (a.n_reads + 255) / 256;
@@ -335,6 +362,6 @@ cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms
   return cudaGetLastError();
 }
 
-uint64_t supermer_tiles(uint64_t n_bases) { return (n_bases + kTile - 1) / kTile; }
+uint64_t supermer_tiles(uint64_t n_bases) { return (n_bases + kSTile - 1) / kSTile; }
 
 }  // namespace gerbil
