@@ -257,21 +257,33 @@ def main() -> None:
     # ---- roofline of the dominant kernel (count, step d) ----------------------------------
     peak, peak_src = _peaks()
     W = st["W"]
-    slot = 8 + 8 * W
+    # table bytes per slot: 16 B inline slots for k <= 46, else the chunked bucket / 4
+    slot = 16 if K <= 46 else (32 + 32 * ((K + 30) // 31)) / 4
     n_count = max(per_kernel["count"][1], 1)
     avg_count_ms = per_kernel["count"][0] / n_count
-    # algorithmic bytes per step of the count kernel: descriptors
-    # (8 B/super-mer), packed super-mer bases (0.25 B/base), and one write of every claimed
-    # table slot (S B per distinct k-mer).
+    # algorithmic bytes per step of the count kernel (SURVEY.md §8(d) stream model restricted to
+    # this kernel): descriptors (8 B/super-mer), packed super-mer bases
+    # (0.25 B/base), and one write of every claimed table slot (slot B per distinct k-mer).
     sm_bases = st["valid_windows"] + st["supermers"] * (K - 1)
     count_bytes_step = 8 * st["supermers"] + 0.25 * sm_bases + slot * st["distinct"]
     bytes_per_launch = count_bytes_step / max(st["launches_count"], 1)
     achieved = bytes_per_launch / (avg_count_ms / 1e3) / 1e9 if avg_count_ms > 0 else None
-    roofline = {"bound": "hbm", "kernel": "count_kernel<W>", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_source": peak_src,
-                "bytes_model": "8*supermers + 0.25*supermer_bases + (8+8W)*distinct per step",
+    # ncu-measured DRAM bytes per launch of this kernel (profiles/, same workload): traffic
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        if tj.get("workload") == WORKLOAD_NAME and tj.get("kernel") == "count_inline_kernel":
+            traffic = tj.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": "count_inline_kernel<2,true>", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src,
+                "bytes_model": f"8*supermers + 0.25*supermer_bases + {slot:g}*distinct per step",
+                "algorithmic_bytes_per_launch": bytes_per_launch,
                 "avg_launch_ms": avg_count_ms, "launches_per_step": st["launches_count"],
-                "share_of_step": per_kernel["count"][0] / args.steps / ms}
+                "share_of_step": per_kernel["count"][0] / args.steps / ms,
+                "note": "L2-resident table: the kernel is bound by L2 sector throughput/latency "
+                        "(ncu lts throughput ~55% of peak), not HBM; see DESIGN.md §4"}
 
     # ---- end to end through the C ABI with host buffers -----------------------------------
     e2e = None
