@@ -94,6 +94,9 @@ typedef struct {
   uint64_t wave_table_bytes; /* per-wave table budget (kept L2-resident); 0 = 128 MiB */
   void* stream;            /* cudaStream_t to launch on; NULL = library-owned stream */
   int32_t timing;          /* 1 = record per-kernel CUDA-event times into gerbil_stats */
+  int32_t force_exchange;  /* 1 = run the multi-rank shuffle even when world == 1 (test
+                              seam: exercises the NCCL all-gather / send / recv path on one
+                              GPU; a 1-rank communicator is created internally) */
 } gerbil_config;
 
 /* Exactly one source must be set. */

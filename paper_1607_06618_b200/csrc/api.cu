@@ -14,6 +14,7 @@
 // atomics are served by L2 and HBM sees the streaming traffic only.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -391,7 +392,7 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     unsigned long long* h = ctx->hist.as<unsigned long long>();
     a.bin_windows = h;
     a.bin_supermers = h + B;
-    a.bin_words = ctx->world > 1 ? h + 2 * B : nullptr;
+    a.bin_words = ctx->comm ? h + 2 * B : nullptr;
     CK(ctx->tile_first.ensure(std::max<uint64_t>(supermer_tiles(n_bases), 1) * 8));
     {
       Timer tm(ctx, K_SUPERMER);
@@ -451,7 +452,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   std::vector<uint32_t> owned;
   const uint64_t* stream_codes = codes;
   uint64_t owned_windows = 0;
-  if (ctx->world <= 1) {
+  if (!ctx->comm) {
     // (c) local: group descriptors by bin
     for (uint32_t b = 0; b < B; ++b) {
       bin_win[b] = hist[b];
@@ -700,9 +701,19 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
     delete ctx;
     return GERBIL_E_CUDA;
   }
-  if (cfg.world > 1) {
+  if (cfg.world > 1 || cfg.force_exchange) {
     std::string err;
-    ctx->comm = make_comm(cfg.comm_backend, cfg.nccl_unique_id, cfg.rank, cfg.world, err);
+    unsigned char own_id[128] = {0};
+    const void* id = cfg.nccl_unique_id;
+    if (!id) {  // world == 1 with force_exchange: a private 1-rank group
+      if (cfg.comm_backend == 0 && !nccl_get_unique_id(own_id, err)) {
+        gerbil_finalize(ctx);
+        return GERBIL_E_NCCL;
+      }
+      if (cfg.comm_backend != 0) snprintf((char*)own_id, sizeof own_id, "gerbil-self-%p", (void*)ctx);
+      id = own_id;
+    }
+    ctx->comm = make_comm(cfg.comm_backend, id, cfg.rank, cfg.world, err);
     if (!ctx->comm) {
       gerbil_finalize(ctx);
       return GERBIL_E_NCCL;

@@ -47,6 +47,7 @@ class Config(C.Structure):
         ("wave_table_bytes", C.c_uint64),
         ("stream", C.c_void_p),
         ("timing", C.c_int32),
+        ("force_exchange", C.c_int32),
     ]
 
 
@@ -203,7 +204,7 @@ class Gerbil:
                  world: int = 1, unique_id: bytes | None = None, comm_backend: int = 0,
                  max_probes: int = 0, distinct_ratio: float = 0.0, target_load: float = 0.0,
                  wave_table_bytes: int = 0, host_threads: int = 0, stream: int | None = None,
-                 timing: bool = False):
+                 timing: bool = False, force_exchange: bool = False):
         cfg = Config()
         _lib.gerbil_config_default(C.byref(cfg))
         cfg.device = device
@@ -221,6 +222,7 @@ class Gerbil:
         cfg.host_threads = host_threads
         cfg.stream = stream
         cfg.timing = 1 if timing else 0
+        cfg.force_exchange = 1 if force_exchange else 0
         h = C.c_void_p()
         st = _lib.gerbil_init(C.byref(cfg), C.byref(h))
         if st != OK:

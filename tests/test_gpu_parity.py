@@ -258,6 +258,21 @@ def test_usage_errors(G):
         assert e.value.status == G.E_IO
 
 
+# ---- the exchange path on one GPU: NCCL (1-rank communicator) and loopback -------------
+@pytest.mark.parametrize("backend", [0, 1])
+def test_forced_exchange_single_rank(G, backend):
+    # world = 1 but the full multi-rank shuffle runs: histogram all-gather, LPT owners,
+    # pack into the send buffer, grouped send/recv to self, regroup of received super-mers
+    w = synth.Workload(seed=43, genome_len=30_000, read_len=120, n_reads=4000, err=0.004, nrate=0.001)
+    text = synth.fastx(w, synth.FASTQ)
+    for k in (33, 65):
+        ref = oracle.count(text, k)
+        keys, counts, st = _gpu_count_text(G, text, k, 7, 1, force_exchange=True, comm_backend=backend,
+                                           n_bins=128)
+        compare(keys, counts, k, ref)
+        assert st["count_sum"] == ref.windows
+
+
 # ---- multi-rank shard logic: loopback group (P virtual ranks on one GPU) ---------------
 @pytest.mark.parametrize("P", [2, 3, 4])
 def test_loopback_ranks_parity(G, P):
