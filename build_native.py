@@ -26,7 +26,7 @@ NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-rela
            "-I" + os.path.join(ROOT, "include")] + ARCH
 
 GERBIL_CU = ["supermer.cu", "shuffle.cu", "count.cu", "compact.cu", "comm.cu", "api.cu"]
-GERBIL_CPP = ["reader.cpp"]
+GERBIL_CPP = ["reader.cpp", "output.cpp"]
 
 LIB_GERBIL = os.path.join(LIBDIR, "libgerbil.so")
 LIB_SYNTH = os.path.join(ROOT, "synth", "libsynth.so")

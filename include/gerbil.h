@@ -97,7 +97,17 @@ typedef struct {
   int32_t force_exchange;  /* 1 = run the multi-rank shuffle even when world == 1 (test
                               seam: exercises the NCCL all-gather / send / recv path on one
                               GPU; a 1-rank communicator is created internally) */
+  int32_t disable_normalization; /* 1 = `-d`: count each k-mer as it occurs;
+                                    x and rc(x) are different k-mers. 0 = canonical (default) */
 } gerbil_config;
+
+/* Result encodings (App. C). */
+typedef enum {
+  GERBIL_FMT_BINARY = 0, /* per k-mer: count < 255 → 1 byte; else 0xFF + 4-byte big-endian
+                            count; then ceil(k/4) bytes, 4 bases per byte A=00 C=01 G=10 T=11,
+                            first base in the most significant bits, pad bits 0 */
+  GERBIL_FMT_CSV = 1     /* `-x h` human readable: one "KMER,COUNT\n" line per k-mer */
+} gerbil_format;
 
 /* Exactly one source must be set. */
 typedef struct {
@@ -181,6 +191,17 @@ gerbil_status gerbil_pack_reads(const gerbil_reads* reads, int32_t threads,
  * Fails with GERBIL_E_USAGE if capacity < n. */
 gerbil_status gerbil_fetch(gerbil_ctx* ctx, uint64_t* kmers, uint32_t* counts,
                            uint64_t capacity, uint64_t* n_out, int sorted);
+
+/* Encodes this rank's results (count >= min_count) in `format` (gerbil_format)
+ * into out[capacity] bytes; out == NULL → only *n_bytes is written (two-call
+ * pattern). sorted != 0 → ascending k-mer order (the CSV of PAPER.md:521 is
+ * for small data sets; SPEC.md:475 sorts it). GERBIL_E_USAGE if capacity is
+ * too small, GERBIL_E_STATE before a successful count. */
+gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted, uint8_t* out,
+                                    uint64_t capacity, uint64_t* n_bytes);
+
+/* Same, written to a file (GERBIL_E_IO if it cannot be written). */
+gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted);
 
 /* Device-side view of this rank's results (valid until the next count). */
 gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers,

@@ -111,3 +111,14 @@ def supermers(seq: bytes, k: int, m: int, ordering: int = LEX, symmetric: bool =
     buf = C.create_string_buffer(max(need, 1))
     L.oracle_supermers(seq, len(seq), k, m, ordering, 1 if symmetric else 0, buf, need)
     return [s for s in buf.raw[:need].split(b"\n") if s]
+
+
+def encode_entry(kmer: bytes, count: int) -> bytes:
+    """App. C output record of one (k-mer, count) pair."""
+    L = lib()
+    L.oracle_encode_entry.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, C.c_char_p]
+    L.oracle_encode_entry.restype = C.c_uint64
+    n = L.oracle_encode_entry(kmer, len(kmer), count, None)
+    buf = C.create_string_buffer(n)
+    L.oracle_encode_entry(kmer, len(kmer), count, buf)
+    return buf.raw[:n]

@@ -328,6 +328,44 @@ void oracle_canonical(const char* x, uint32_t n, char* out) {
   memcpy(out, c.data(), n);
 }
 
+/* One output record, App. C: "The counter of each occuring
+ * k-mer is stored in binary form, followed by the corresponding byte-encoded
+ * k-mer. Each four bases of a k-mer are encoded in one single byte. We encode A
+ * with 00, C with 01, G with 10 and T with 11 ... only one byte for counters
+ * less than 255. A counter greater than or equal to 255 is encoded in five
+ * bytes. In the latter case, all bits of the first byte are set to 1. The
+ * remaining four bytes contain the counter in a conventional 32-bit unsigned
+ * integer." Byte order of the counter and bit order of the bases follow the
+ * worked examples; the undefined pad bits X are written 0
+ * (SPEC.md:54). Returns the record length; writes it to out if non-NULL. */
+uint64_t oracle_encode_entry(const char* kmer, uint32_t k, uint64_t count, uint8_t* out) {
+  std::vector<uint8_t> rec;
+  if (count < 255) {
+    rec.push_back((uint8_t)count);
+  } else {
+    rec.push_back(0xFF);
+    for (int shift = 24; shift >= 0; shift -= 8) rec.push_back((uint8_t)((count >> shift) & 0xFF));
+  }
+  for (uint32_t i = 0; i < k; i += 4) {
+    uint8_t byte = 0;
+    for (uint32_t j = 0; j < 4; ++j) {
+      uint8_t code = 0; /* pad bases beyond k: 00 */
+      if (i + j < k) {
+        switch (kmer[i + j]) {
+          case 'A': code = 0; break;
+          case 'C': code = 1; break;
+          case 'G': code = 2; break;
+          case 'T': code = 3; break;
+        }
+      }
+      byte = (uint8_t)((byte << 2) | code);
+    }
+    rec.push_back(byte);
+  }
+  if (out) memcpy(out, rec.data(), rec.size());
+  return rec.size();
+}
+
 /* Minimizer m-mer of one k-mer (ordering 0 = KMC2, 1 = LEX). */
 void oracle_minimizer(const char* kmer, uint32_t k, uint32_t m, int ordering,
                       int symmetric, char* out) {

@@ -29,6 +29,7 @@
 #include "comm.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "output.h"
 #include "reader.h"
 #include "table.cuh"
 #include "table_inline.cuh"
@@ -270,7 +271,8 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     for (size_t w = 0; w < waves.size(); ++w) {
       t.nb = waves[w].nb;
       CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t,
-                  ctx->wave_distinct.as<unsigned long long>() + nw + w};
+                  ctx->wave_distinct.as<unsigned long long>() + nw + w,
+                  ctx->cfg.disable_normalization ? 0u : 1u};
       {
         Timer tm(ctx, K_COUNT);
         CK(launch_count(a, W, ctx->sms, ctx->stream));
@@ -864,6 +866,38 @@ gerbil_status gerbil_fetch(gerbil_ctx* ctx, uint64_t* kmers, uint32_t* counts, u
     memcpy(kmers, kk.data(), n * W * 8);
     if (counts) memcpy(counts, cc.data(), n * 4);
   }
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted, uint8_t* out,
+                                    uint64_t capacity, uint64_t* n_bytes) {
+  if (!ctx || !n_bytes) return GERBIL_E_USAGE;
+  if (format != GERBIL_FMT_BINARY && format != GERBIL_FMT_CSV) return fail(ctx, GERBIL_E_USAGE, "unknown format");
+  if (!ctx->have_result) return fail(ctx, GERBIL_E_STATE, "no successful count yet");
+  const uint64_t n = ctx->n_out, W = ctx->W;
+  std::vector<uint64_t> keys(std::max<uint64_t>(n * W, 1));
+  std::vector<uint32_t> counts(std::max<uint64_t>(n, 1));
+  uint64_t got = 0;
+  CKS(gerbil_fetch(ctx, keys.data(), counts.data(), n, &got, sorted));
+  const uint64_t need = encode_results(format, keys.data(), counts.data(), got, ctx->k, (uint32_t)W, nullptr,
+                                       ctx->cfg.host_threads);
+  *n_bytes = need;
+  if (!out) return GERBIL_OK;
+  if (capacity < need) return fail(ctx, GERBIL_E_USAGE, "capacity too small");
+  encode_results(format, keys.data(), counts.data(), got, ctx->k, (uint32_t)W, out, ctx->cfg.host_threads);
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted) {
+  if (!ctx || !path) return GERBIL_E_USAGE;
+  uint64_t nb = 0;
+  CKS(gerbil_encode_results(ctx, format, sorted, nullptr, 0, &nb));
+  std::vector<uint8_t> buf(std::max<uint64_t>(nb, 1));
+  CKS(gerbil_encode_results(ctx, format, sorted, buf.data(), nb, &nb));
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(ctx, GERBIL_E_IO, std::string(path) + ": cannot open for writing");
+  const bool ok = fwrite(buf.data(), 1, nb, f) == nb;
+  if (fclose(f) != 0 || !ok) return fail(ctx, GERBIL_E_IO, std::string(path) + ": write failed");
   return GERBIL_OK;
 }
 

@@ -107,8 +107,11 @@ __global__ void __launch_bounds__(kThreads) count_kernel(CountArgs a) {
       for (int u = 0; u < U; ++u) {
         uint64_t x[W], r[W];
         extract_kmer<W>(a.codes, act[u] ? q[u] : 0ull, a.k, x);
-        reverse_complement<W>(x, a.k, r);
-        const bool use_r = key_less<W>(r, x);
+        bool use_r = false;
+        if (a.canonical) {  // warp-uniform
+          reverse_complement<W>(x, a.k, r);
+          use_r = key_less<W>(r, x);
+        }
 #pragma unroll
         for (int v = 0; v < W; ++v) c[u][v] = use_r ? r[v] : x[v];
         to_chunks<W, WP>(c[u], ch[u]);

@@ -204,8 +204,11 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
       } else {
         extract_kmer<W>(a.codes, act ? pj + (i - ej) : 0ull, a.k, x);
       }
-      reverse_complement<W>(x, a.k, r);
-      const bool use_r = key_less<W>(r, x);
+      bool use_r = false;
+      if (a.canonical) {  // warp-uniform
+        reverse_complement<W>(x, a.k, r);
+        use_r = key_less<W>(r, x);
+      }
 #pragma unroll
       for (int v = 0; v < W; ++v) c[v] = use_r ? r[v] : x[v];
       uint64_t ch[2];

@@ -76,6 +76,7 @@ struct CountArgs {
   uint32_t k;
   TableArgs t;
   unsigned long long* work;  // zeroed per launch: dynamic chunk counter
+  uint32_t canonical;        // 1 = count min(x, rc x); 0 = `-d`
 };
 cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
 

@@ -20,6 +20,7 @@ if not os.path.exists(_LIB_PATH):
 _lib = C.CDLL(_LIB_PATH)
 
 OK, E_USAGE, E_IO, E_INTERNAL, E_NOMEM, E_CUDA, E_NCCL, E_STATE = range(8)
+FMT_BINARY, FMT_CSV = 0, 1
 ORDER_KMC2, ORDER_LEX = 0, 1
 
 
@@ -48,6 +49,7 @@ class Config(C.Structure):
         ("stream", C.c_void_p),
         ("timing", C.c_int32),
         ("force_exchange", C.c_int32),
+        ("disable_normalization", C.c_int32),
     ]
 
 
@@ -115,18 +117,20 @@ _lib.gerbil_get_stats.argtypes = [_P, C.POINTER(Stats)]
 _lib.gerbil_last_error.argtypes = [_P]
 _lib.gerbil_last_error.restype = C.c_char_p
 _lib.gerbil_finalize.argtypes = [_P]
+_lib.gerbil_encode_results.argtypes = [_P, C.c_int32, C.c_int, _P, C.c_uint64, _U64P]
+_lib.gerbil_write_results.argtypes = [_P, C.c_char_p, C.c_int32, C.c_int]
 _lib.gerbil_debug_supermers.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32,
                                         _P, _P, _P, _P, C.c_uint64, _U64P]
 for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count_device",
            "gerbil_count_host_packed", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
-           "gerbil_get_stats", "gerbil_debug_supermers"):
+           "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = [
     "gerbil_config_default", "gerbil_init", "gerbil_nccl_unique_id", "gerbil_count",
     "gerbil_count_device", "gerbil_count_host_packed", "gerbil_pack_reads", "gerbil_fetch",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
-    "gerbil_debug_supermers",
+    "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
 ]
 
 
@@ -204,7 +208,7 @@ class Gerbil:
                  world: int = 1, unique_id: bytes | None = None, comm_backend: int = 0,
                  max_probes: int = 0, distinct_ratio: float = 0.0, target_load: float = 0.0,
                  wave_table_bytes: int = 0, host_threads: int = 0, stream: int | None = None,
-                 timing: bool = False, force_exchange: bool = False):
+                 timing: bool = False, force_exchange: bool = False, canonical: bool = True):
         cfg = Config()
         _lib.gerbil_config_default(C.byref(cfg))
         cfg.device = device
@@ -223,6 +227,7 @@ class Gerbil:
         cfg.stream = stream
         cfg.timing = 1 if timing else 0
         cfg.force_exchange = 1 if force_exchange else 0
+        cfg.disable_normalization = 0 if canonical else 1
         h = C.c_void_p()
         st = _lib.gerbil_init(C.byref(cfg), C.byref(h))
         if st != OK:
@@ -286,6 +291,17 @@ class Gerbil:
         self._check(_lib.gerbil_fetch(self._h, _ptr(keys), _ptr(counts), keys.shape[0], C.byref(got),
                                       1 if sorted else 0))
         return keys[: got.value], counts[: got.value]
+
+    def encode_results(self, fmt: int = FMT_BINARY, sorted: bool = True) -> bytes:
+        """Results in the paper's binary format (App. C) or as CSV (`-x h`)."""
+        n = C.c_uint64()
+        self._check(_lib.gerbil_encode_results(self._h, fmt, 1 if sorted else 0, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self._check(_lib.gerbil_encode_results(self._h, fmt, 1 if sorted else 0, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def write_results(self, path: str, fmt: int = FMT_BINARY, sorted: bool = True) -> None:
+        self._check(_lib.gerbil_write_results(self._h, path.encode(), fmt, 1 if sorted else 0))
 
     def results_device(self) -> tuple[int, int, int, int]:
         """(kmers_ptr, counts_ptr, n, W) of the device-resident results."""

@@ -303,3 +303,35 @@ def test_loopback_ranks_parity(G, P):
     compare(keys[order], counts[order], 56, ref)
     assert sum(r[2]["count_sum"] for r in results) == ref.windows
     assert all(r[2]["bytes_recv"] > 0 for r in results)
+
+
+# ---- NEXT(2): -d non-canonical mode and the paper's output encodings ----------------------
+@pytest.mark.parametrize("k", [12, 31, 32, 33, 40, 64, 65, 100])
+def test_parity_non_canonical(G, k):
+    # PAPER.md:483 `-d`: a k-mer and its reverse complement are different k-mers
+    w = synth.Workload(seed=300 + k, genome_len=20_000, read_len=150, n_reads=1500, err=0.004, nrate=0.001)
+    text = synth.fastx(w, synth.FASTQ) + b"@t\n" + b"T" * 80 + b"\n+\n" + b"I" * 80 + b"\n"
+    ref = oracle.count(text, k, 1, canonical=False)
+    keys, counts, st = _gpu_count_text(G, text, k, 7, 1, canonical=False, n_bins=32)
+    compare(keys, counts, k, ref)
+    assert st["count_sum"] == ref.windows
+
+
+@pytest.mark.parametrize("k,min_count", [(28, 1), (40, 2), (65, 1)])
+def test_binary_and_csv_output(G, k, min_count, tmp_path):
+    # App. C records byte-exact against the oracle's encoder, counts >= 255
+    # exercised by a repeated read; CSV (`-x h`) line-exact
+    w = synth.Workload(seed=7, genome_len=5_000, read_len=100, n_reads=2000, err=0.002)
+    rep = b"ACGTTGCA" * 12
+    text = synth.fastx(w, synth.FASTQ) + b"".join(b"@r\n" + rep + b"\n+\n" + b"I" * len(rep) + b"\n"
+                                                  for _ in range(300))
+    ref = oracle.count(text, k, min_count)
+    with G.Gerbil() as g:
+        g.count(k, 7, min_count, text=text)
+        binary = g.encode_results(G.FMT_BINARY, sorted=True)
+        csv = g.encode_results(G.FMT_CSV, sorted=True)
+        g.write_results(str(tmp_path / "out.bin"), G.FMT_BINARY, sorted=True)
+    assert binary == b"".join(oracle.encode_entry(x, c) for x, c in zip(ref.kmers, ref.counts))
+    assert max(ref.counts) >= 255
+    assert csv == b"".join(x + b"," + str(c).encode() + b"\n" for x, c in zip(ref.kmers, ref.counts))
+    assert (tmp_path / "out.bin").read_bytes() == binary

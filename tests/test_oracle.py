@@ -185,6 +185,14 @@ def test_de_bruijn_closed_form(k):
     assert res.windows == 4**k
 
 
+def test_de_bruijn_non_canonical():
+    # `-d`: without normalization every k-mer of B(4,8) is its own key, count 1
+    s = _de_bruijn(8)
+    res = oracle.count(b">db\n" + s + b"\n", 8, canonical=False)
+    assert len(res.kmers) == 4**8 and set(res.counts) == {1}
+    assert oracle.count(b">t\n" + b"T" * 40 + b"\n", 32, canonical=False).as_dict() == {b"T" * 32: 9}
+
+
 def test_sum_counts_equals_valid_windows():
     # Σ counts (min_count=1) = Σ over N-free fragments of max(0, |F|-k+1)
     rnd = random.Random(2)
@@ -311,3 +319,20 @@ def test_sampled_equals_filtered_full():
     expect = {x: c for x, c in full.as_dict().items() if oracle.sample_keep(x, 16)}
     assert samp.as_dict() == expect and len(expect) > 0
     assert samp.windows == full.windows
+
+
+# ---- App. C output encoding (NEXT(2)) ------------------------------------------------
+def test_output_encoding_paper_examples():
+    # PAPER.md:517-518 worked examples (tests/golden/appendix_bytes.txt)
+    for row in _golden("appendix_bytes.txt"):
+        count, kmer, hexrec = row.split()
+        assert oracle.encode_entry(kmer.encode(), int(count)) == bytes.fromhex(hexrec)
+
+
+def test_output_encoding_boundaries():
+    # "only one byte for counters less than 255. A counter greater than or equal to 255 is
+    # encoded in five bytes"; ceil(k/4) k-mer bytes, pad bits 0
+    assert oracle.encode_entry(b"A" * 8, 254) == bytes([254, 0, 0])
+    assert oracle.encode_entry(b"A" * 8, 255) == bytes([0xFF, 0, 0, 0, 255, 0, 0])
+    assert oracle.encode_entry(b"T" * 9, 1) == bytes([1, 0xFF, 0xFF, 0xC0])
+    assert oracle.encode_entry(b"ACGT", 2**32 - 1) == bytes([0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0x1B])
