@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
            "-I" + os.path.join(ROOT, "include")] + ARCH
 
-GERBIL_CU = ["supermer.cu", "shuffle.cu", "count.cu", "compact.cu", "comm.cu", "api.cu"]
+GERBIL_CU = ["supermer.cu", "supermer_reads.cu", "shuffle.cu", "count.cu", "compact.cu", "comm.cu", "api.cu"]
 GERBIL_CPP = ["reader.cpp", "output.cpp"]
 
 LIB_GERBIL = os.path.join(LIBDIR, "libgerbil.so")

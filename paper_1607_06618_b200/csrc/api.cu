@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -68,7 +69,19 @@ struct DevBuf {
 struct Counters {
   unsigned long long n_supermers, n_windows, ovf_n, out_n, sum_counts, distinct;
   unsigned long long probe[4];
+  unsigned long long read_work;  // dynamic read counter of supermer_reads_kernel
 };
+
+// Step-(b) kernel choice: the tile kernel (supermer.cu) by default — on B200 it
+// beat the read-per-lane kernel (supermer_reads.cu: 49 vs 40 ms on C1, smem
+// rings cap it at 10 warps/SM); GERBIL_SUPERMER_KERNEL=reads selects the latter
+// where it applies (tests run both).
+bool use_reads_kernel(uint32_t k, uint32_t m, uint64_t n_bases, uint64_t n_reads) {
+  const char* e = getenv("GERBIL_SUPERMER_KERNEL");
+  if (e && strcmp(e, "reads") == 0) return n_reads > 0 && k - m + 1 <= 64;
+  (void)n_bases;
+  return false;
+}
 
 enum Kind { K_SUPERMER, K_SHUFFLE, K_COUNT, K_COMPACT, K_OVERFLOW, K_H2D, K_NKIND };
 
@@ -395,8 +408,11 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     a.bin_windows = h;
     a.bin_supermers = h + B;
     a.bin_words = ctx->comm ? h + 2 * B : nullptr;
-    CK(ctx->tile_first.ensure(std::max<uint64_t>(supermer_tiles(n_bases), 1) * 8));
-    {
+    if (use_reads_kernel(k, m, n_bases, n_reads)) {
+      Timer tm(ctx, K_SUPERMER);
+      CK(launch_supermer_reads(a, &dc->read_work, ctx->sms, ctx->stream));
+    } else {
+      CK(ctx->tile_first.ensure(std::max<uint64_t>(supermer_tiles(n_bases), 1) * 8));
       Timer tm(ctx, K_SUPERMER);
       CK(launch_supermer(a, ctx->tile_first.as<uint64_t>(), ctx->sms, ctx->stream));
     }

@@ -25,6 +25,10 @@ struct SupermerArgs {
   unsigned long long* bin_supermers; // [n_bins]
   unsigned long long* bin_words;     // [n_bins] payload words (multi-GPU) or nullptr
 };
+// Read-per-lane variant (supermer_reads.cu) for w = k-m+1 <= 64 and reads of
+// <= 4096 bases on average; `work` is one device counter.
+bool supermer_reads_applicable(uint32_t k, uint32_t m, uint64_t n_bases, uint64_t n_reads);
+cudaError_t launch_supermer_reads(const SupermerArgs& a, unsigned long long* work, int sms, cudaStream_t s);
 // tile_first: scratch of supermer_tiles(n_bases) u64 entries.
 cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms, cudaStream_t s);
 uint64_t supermer_tiles(uint64_t n_bases);

@@ -204,8 +204,10 @@ def test_repeated_calls_and_ratio_adaptation(G):
 
 
 # ---- step (b) properties ----------------------------------------------------------------
-def test_fig1_supermers_on_gpu(G):
+@pytest.mark.parametrize("kernel", ["tile", "reads"])
+def test_fig1_supermers_on_gpu(G, kernel, monkeypatch):
     # PAPER.md:58 Fig. 1 with the lexicographic ordering (strand-symmetric gives the same cuts)
+    monkeypatch.setenv("GERBIL_SUPERMER_KERNEL", kernel)
     p = G.pack_reads(text=b">fig1\nCAAGAACAGTG\n")
     with G.Gerbil(ordering=G.ORDER_LEX, n_bins=4) as g:
         pos, nwin, b, mu = g.debug_supermers(p, 4, 3)
@@ -214,8 +216,31 @@ def test_fig1_supermers_on_gpu(G):
     assert sms == [b"CAAGA", b"AGAA", b"GAACA", b"ACAG", b"CAGTG"]
 
 
+@pytest.mark.parametrize("kernel", ["tile", "reads"])
+@pytest.mark.parametrize("k", [12, 28, 40, 56, 65])
+def test_both_supermer_kernels_parity(G, kernel, k, monkeypatch):
+    # step (b) has a tile kernel and a read-per-lane kernel (w <= 64); both must give the
+    # oracle's histogram on reads with N runs, varied lengths, reads shorter than k
+    monkeypatch.setenv("GERBIL_SUPERMER_KERNEL", kernel)
+    rnd = random.Random(k)
+    reads = []
+    for _ in range(3000):
+        r = bytearray(rnd.choice(b"ACGT") for _ in range(rnd.randint(1, 400)))
+        for _ in range(rnd.randint(0, 3)):
+            p = rnd.randrange(len(r))
+            r[p:p + 3] = b"NNN"[: len(r[p:p + 3])]
+        reads.append(bytes(r))
+    text = b"".join(b">r\n" + r + b"\n" for r in reads)
+    ref = oracle.count(text, k)
+    keys, counts, st = _gpu_count_text(G, text, k, 7, 1, n_bins=64)
+    compare(keys, counts, k, ref)
+    assert st["valid_windows"] == ref.windows
+
+
+@pytest.mark.parametrize("kernel", ["tile", "reads"])
 @pytest.mark.parametrize("k,m,ordering", [(28, 7, 0), (40, 9, 0), (65, 11, 1), (200, 15, 0), (9, 3, 0)])
-def test_supermer_properties(G, k, m, ordering):
+def test_supermer_properties(G, k, m, ordering, kernel, monkeypatch):
+    monkeypatch.setenv("GERBIL_SUPERMER_KERNEL", kernel)
     w = synth.Workload(seed=31, genome_len=10_000, read_len=300, n_reads=200, err=0.01, nrate=0.003)
     text = synth.fastx(w, synth.RAW)
     p = G.pack_reads(text=text)
