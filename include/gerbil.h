@@ -88,7 +88,7 @@ typedef struct {
   int32_t ordering;        /* gerbil_ordering; 0 = KMC2 */
   uint64_t device_mem_cap; /* bytes of device memory the library may allocate; 0 = auto (`-e`) */
   int32_t host_threads;    /* host reader threads; 0 = all cores (`-t`) */
-  uint32_t max_probes;     /* θ in buckets; 0 = 32 */
+  uint32_t max_probes;     /* θ in buckets; 0 = 32; capped at 2^20 */
   double distinct_ratio;   /* initial ρ̂ = distinct/total estimate; 0 = 0.5 */
   double target_load;      /* α: table load factor target; 0 = 0.7 */
   uint64_t wave_table_bytes; /* per-wave table budget (kept L2-resident); 0 = 128 MiB */
@@ -137,7 +137,9 @@ typedef struct {
   uint64_t bytes_sent, bytes_recv; /* step (c) NVLink traffic of this rank */
   double ratio_used;         /* ρ̂ used to size this call's tables */
   double ratio_observed;     /* max over waves of distinct / windows */
-  /* per-stage device milliseconds (timing=1): */
+  /* per-stage device milliseconds (timing=1). Steps (d)+(e) run in two
+     overlapping wave lanes by default: ms_count is then the span of both
+     steps and ms_compact is 0 (GERBIL_WAVE_LANES=1: separate, serial). */
   double ms_h2d, ms_supermer, ms_shuffle, ms_count, ms_compact, ms_overflow, ms_total;
   /* host reader (step a) wall milliseconds */
   double ms_reader;

@@ -103,6 +103,8 @@ struct gerbil_ctx {
   int device = 0, sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t lane_stream = nullptr;             // second wave lane (steps d+e)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   bool poisoned = false;
   std::string err;
   double rho = 0.5;
@@ -110,7 +112,7 @@ struct gerbil_ctx {
   int rank = 0, world = 1;
   // device buffers
   DevBuf in_codes, in_nmask, in_rstart;  // uploads of host batches
-  DevBuf desc_pre, bin_pre, mu_dbg, desc_sorted, tile_first;
+  DevBuf desc_pre, bin_pre, mu_dbg, desc_sorted, rs_bits;
   DevBuf counters;
   DevBuf hist;  // [3][B] windows, super-mers, payload words (ull)
   DevBuf hist_all, cursor, cursor2, seg_base;
@@ -126,6 +128,7 @@ struct gerbil_ctx {
   std::vector<TimedEvent> evs;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  uint32_t n_launch[K_NKIND] = {0};
 };
 
 namespace {
@@ -160,21 +163,35 @@ cudaEvent_t get_event(gerbil_ctx* ctx) {
   return ctx->ev_pool[ctx->ev_used++];
 }
 
-struct Timer {  // CUDA-event pair around one launch when timing is on
+// Counts one launch of `kind`; with timing on and `timed`, a CUDA-event pair
+// brackets it on stream `st`. A span timer (launches = 0) brackets a phase.
+struct Timer {
   gerbil_ctx* ctx;
+  cudaStream_t st;
   cudaEvent_t b = nullptr;
-  Timer(gerbil_ctx* c, int kind) : ctx(c) {
-    if (ctx->cfg.timing) {
+  Timer(gerbil_ctx* c, int kind, cudaStream_t s = nullptr, bool timed = true, uint32_t launches = 1)
+      : ctx(c), st(s ? s : c->stream) {
+    ctx->n_launch[kind] += launches;
+    if (ctx->cfg.timing && timed) {
       cudaEvent_t a = get_event(ctx);
       b = get_event(ctx);
-      cudaEventRecord(a, ctx->stream);
+      cudaEventRecord(a, st);
       ctx->evs.push_back({kind, a, b});
     }
   }
   ~Timer() {
-    if (b) cudaEventRecord(b, ctx->stream);
+    if (b) cudaEventRecord(b, st);
   }
 };
+
+// Wave lanes: with 2, consecutive waves alternate between two half-budget
+// tables on two streams, so one wave's compaction and launch tail overlap the
+// next wave's counting (GERBIL_WAVE_LANES=1 restores the serial schedule).
+int wave_lanes() {
+  const char* e = getenv("GERBIL_WAVE_LANES");
+  if (e && *e) return atoi(e) <= 1 ? 1 : 2;
+  return 2;
+}
 
 gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_count) {
   if (!ctx) return GERBIL_E_USAGE;
@@ -216,7 +233,9 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   const uint64_t bb = table_inline(k) ? kInlineBucketBytes : table_bucket_bytes(k);
   const double slot_bytes = (double)bb / kSlotsPerBucket;
   const double alpha = ctx->cfg.target_load;
-  const uint32_t theta = ctx->cfg.max_probes;
+  const uint32_t theta = std::min<uint32_t>(ctx->cfg.max_probes, 1u << 20);  // probe counters are 24-bit
+  const int lanes = wave_lanes();
+  const double budget = (double)ctx->cfg.wave_table_bytes / lanes;  // per-lane table bytes
   Counters& hc = *ctx->h_counters;
   for (int attempt = 0;; ++attempt) {
     const double rho = ctx->rho;
@@ -239,7 +258,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
       };
       for (uint32_t b : bins) {
         const double need = rho * (double)bin_win[b] / alpha * slot_bytes;
-        if (open && acc + need > (double)ctx->cfg.wave_table_bytes) close();
+        if (open && acc + need > budget) close();
         if (!open) {
           cur = Wave{bin_off[b], bin_off[b], 0, 0};
           open = true;
@@ -251,7 +270,8 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
       close();
     }
     const uint64_t ovf_cap = std::max<uint64_t>(1 << 16, total_windows / 32);
-    CK(ctx->table.ensure(max_nb * bb));
+    const uint64_t lane_bytes = (max_nb * bb + 255) & ~255ull;
+    CK(ctx->table.ensure(lanes * lane_bytes));
     CK(ctx->ovf.ensure(ovf_cap * W * 8));
     const uint64_t out_cap = out_bound + ovf_cap;
     CK(ctx->out_keys.ensure(out_cap * W * 8));
@@ -259,7 +279,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     // [0, n): distinct per wave; [n, 2n): dynamic work counters of the count launches
     const size_t nw = std::max<size_t>(waves.size(), 1);
     CK(ctx->wave_distinct.ensure(2 * nw * 8));
-    CK(cudaMemsetAsync(ctx->table.p, 0, max_nb * bb, ctx->stream));
+    CK(cudaMemsetAsync(ctx->table.p, 0, lanes * lane_bytes, ctx->stream));
     CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, 2 * nw * 8, ctx->stream));
     Counters* dc = ctx->counters.as<Counters>();
     CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
@@ -281,20 +301,38 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ca.out_n = &dc->out_n;
     ca.sum_counts = &dc->sum_counts;
     ca.distinct = &dc->distinct;
-    for (size_t w = 0; w < waves.size(); ++w) {
-      t.nb = waves[w].nb;
-      CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t,
-                  ctx->wave_distinct.as<unsigned long long>() + nw + w,
-                  ctx->cfg.disable_normalization ? 0u : 1u};
-      {
-        Timer tm(ctx, K_COUNT);
-        CK(launch_count(a, W, ctx->sms, ctx->stream));
+    {
+      // with two lanes the per-launch events would overlap: one span timer
+      // covers steps (d)+(e) and is reported as ms_count (ms_compact = 0)
+      const bool two = lanes > 1 && waves.size() > 1;
+      Timer span(ctx, K_COUNT, ctx->stream, two, 0);
+      if (two) {
+        CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->lane_stream, ctx->fork_ev, 0));
       }
-      ca.nb = waves[w].nb;
-      ca.wave_distinct = ctx->wave_distinct.as<unsigned long long>() + w;
-      {
-        Timer tm(ctx, K_COMPACT);
-        CK(launch_compact(ca, ctx->sms, ctx->stream));
+      for (size_t w = 0; w < waves.size(); ++w) {
+        const int lane = two ? (int)(w & 1) : 0;
+        cudaStream_t st = lane ? ctx->lane_stream : ctx->stream;
+        t.table = ctx->table.as<unsigned char>() + lane * lane_bytes;
+        t.nb = waves[w].nb;
+        CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t,
+                    ctx->wave_distinct.as<unsigned long long>() + nw + w,
+                    ctx->cfg.disable_normalization ? 0u : 1u};
+        {
+          Timer tm(ctx, K_COUNT, st, !two);
+          CK(launch_count(a, W, ctx->sms, st));
+        }
+        ca.table = t.table;
+        ca.nb = waves[w].nb;
+        ca.wave_distinct = ctx->wave_distinct.as<unsigned long long>() + w;
+        {
+          Timer tm(ctx, K_COMPACT, st, !two);
+          CK(launch_compact(ca, ctx->sms, st));
+        }
+      }
+      if (two) {
+        CK(cudaEventRecord(ctx->join_ev, ctx->lane_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
       }
     }
     CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
@@ -337,6 +375,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
       // exactly in a table with room for all of them and θ = every bucket.
       const uint64_t nb2 = std::max<uint64_t>(8, (uint64_t)std::ceil((double)ovf_n / (0.5 * kSlotsPerBucket)));
       CK(ctx->table.ensure(nb2 * bb));
+      t.table = ctx->table.as<unsigned char>();
       CK(cudaMemsetAsync(ctx->table.p, 0, nb2 * bb, ctx->stream));
       // overflow keys must not be overwritten while re-inserted: θ = nb2 never overflows
       TableArgs t2 = t;
@@ -370,7 +409,6 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ctx->stats.distinct = hc.distinct;
     ctx->stats.count_sum = hc.sum_counts;
     ctx->stats.owned_windows = total_windows;
-    ctx->stats.launches_count = 0;
     return GERBIL_OK;
   }
 }
@@ -412,9 +450,9 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
       Timer tm(ctx, K_SUPERMER);
       CK(launch_supermer_reads(a, &dc->read_work, ctx->sms, ctx->stream));
     } else {
-      CK(ctx->tile_first.ensure(std::max<uint64_t>(supermer_tiles(n_bases), 1) * 8));
-      Timer tm(ctx, K_SUPERMER);
-      CK(launch_supermer(a, ctx->tile_first.as<uint64_t>(), ctx->sms, ctx->stream));
+      CK(ctx->rs_bits.ensure(supermer_scratch_words(n_bases) * 8));
+      Timer tm(ctx, K_SUPERMER, nullptr, true, n_reads ? 2u : 1u);  // rs_bits_kernel + supermer_kernel
+      CK(launch_supermer(a, ctx->rs_bits.as<uint64_t>(), ctx->sms, ctx->stream));
     }
     CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -433,6 +471,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   ctx->n_out = 0;
   ctx->evs.clear();
   ctx->ev_used = 0;
+  for (auto& v : ctx->n_launch) v = 0;
   memset(&ctx->stats, 0, sizeof ctx->stats);
   const uint32_t W = key_words(k);
   ctx->W = W;
@@ -640,24 +679,22 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   // timing
   if (ctx->cfg.timing) {
     double ms[K_NKIND] = {0};
-    uint32_t n[K_NKIND] = {0};
     for (auto& e : ctx->evs) {
       float f = 0;
       cudaEventElapsedTime(&f, e.a, e.b);
       ms[e.kind] += f;
-      n[e.kind]++;
     }
     ctx->stats.ms_supermer = ms[K_SUPERMER];
     ctx->stats.ms_shuffle = ms[K_SHUFFLE];
     ctx->stats.ms_count = ms[K_COUNT];
     ctx->stats.ms_compact = ms[K_COMPACT];
     ctx->stats.ms_overflow = ms[K_OVERFLOW];
-    ctx->stats.launches_count = n[K_COUNT];
-    ctx->stats.launches_compact = n[K_COMPACT];
-    uint32_t tot = 0;
-    for (int i = 0; i < K_NKIND; ++i) tot += n[i];
-    ctx->stats.launches_total = tot;
   }
+  // kernel launches of this call (copies are not launches)
+  ctx->stats.launches_count = ctx->n_launch[K_COUNT];
+  ctx->stats.launches_compact = ctx->n_launch[K_COMPACT];
+  ctx->stats.launches_total = ctx->n_launch[K_SUPERMER] + ctx->n_launch[K_SHUFFLE] + ctx->n_launch[K_COUNT] +
+                              ctx->n_launch[K_COMPACT] + ctx->n_launch[K_OVERFLOW];
   ctx->stats.ms_total = wall_ms() - t0;
   ctx->have_result = true;
   return GERBIL_OK;
@@ -714,6 +751,9 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
       ctx->own_stream = true;
     }
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->lane_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_counters, sizeof(Counters));
   if (e != cudaSuccess) {
     delete ctx;
@@ -746,6 +786,12 @@ void gerbil_finalize(gerbil_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   delete ctx->comm;
+  if (ctx->lane_stream) {
+    cudaStreamSynchronize(ctx->lane_stream);
+    cudaStreamDestroy(ctx->lane_stream);
+  }
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->h_counters) cudaFreeHost(ctx->h_counters);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

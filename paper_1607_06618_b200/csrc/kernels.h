@@ -29,9 +29,9 @@ struct SupermerArgs {
 // <= 4096 bases on average; `work` is one device counter.
 bool supermer_reads_applicable(uint32_t k, uint32_t m, uint64_t n_bases, uint64_t n_reads);
 cudaError_t launch_supermer_reads(const SupermerArgs& a, unsigned long long* work, int sms, cudaStream_t s);
-// tile_first: scratch of supermer_tiles(n_bases) u64 entries.
-cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms, cudaStream_t s);
-uint64_t supermer_tiles(uint64_t n_bases);
+// rs_bits: scratch of supermer_scratch_words(n_bases) u64 (read-start bitmap).
+cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t s);
+uint64_t supermer_scratch_words(uint64_t n_bases);
 
 struct ScatterArgs {
   const uint64_t* desc_in;

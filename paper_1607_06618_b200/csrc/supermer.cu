@@ -11,16 +11,19 @@
 // B200 design: the read batch is one packed base
 // stream; a persistent CTA takes tiles of kSTile = 1024 window start positions,
 // independent of read length (100-bp and 10-kbp reads balance the same way).
-//   0. tile_reads_kernel: first read of every tile (one pass over read_start);
-//   1. stage the tile's packed codes, N-mask and read starts in smem
+//   0. rs_bits_kernel: read-start bitmap of the batch (one bit per base, laid
+//      out like the N-mask), so a tile stages read boundaries like N bits;
+//   1. stage the tile's packed codes, N bits and read-start bits in smem
 //      (bitmaps are LSB-first u32 words: position i = bit i%32 of word i/32);
-//   2. keys: thread t rolls the m-mers of key block t (8 consecutive
+//      every thread holds at most one u64 of the NEXT tile in a register,
+//      loaded while the current tile is processed;
+//   2. keys: thread t rolls the m-mers of key block t (kKB = 10 consecutive
 //      positions: one extraction, then 2-bit shifts of f and rc(f)); ordering
 //      key c_j = min(ord f_j, ord rc f_j) (strand-symmetric minimizer,
 //      DESIGN.md Q7); it publishes the block's prefix minima, suffix minima
 //      and minimum;
 //   3. thread t owns windows p = 8t..8t+7: μ_p = min over c[p, p+w) =
-//      min(suffix[p], min of the whole blocks in between, prefix[p+w-1]);
+//      min(suffix[p], min of the whole key blocks in between, prefix[p+w-1]);
 //      validity: no X = N | RS(q+1) bit in [p, p+k-2] and
 //      base p+k-1 not N — one amortised next-set-bit scan per thread;
 //   4. a super-mer starts at a valid window whose predecessor is invalid or has
@@ -46,7 +49,9 @@ constexpr int kKeyLen = kThreads * kKB;     // 1280 >= kSTile + k - m for every 
 constexpr int kKeyBlocks = kThreads;
 constexpr int kCodeWords = (kKeyLen + 16 + 31) / 32 + 2;          // u64 words of 32 bases
 constexpr int kBitWords = ((kSTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
+constexpr int kBitWords64 = kBitWords / 2;
 static_assert(kKeyLen >= (int)kSTile + kMaxK - 1, "key blocks must cover every window");
+static_assert(kCodeWords + 2 * kBitWords64 <= kThreads, "one staged u64 per thread");
 
 __device__ __forceinline__ bool bget(const uint32_t* bm, uint32_t i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
 
@@ -94,19 +99,18 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
-__global__ void tile_reads_kernel(const uint64_t* __restrict__ read_start, uint64_t n_reads,
-                                  uint64_t n_tiles, uint64_t* __restrict__ tile_first) {
-  // tile t starts at p0 = t*kSTile; its first read is the last r with read_start[r] <= p0
+// bit (63 - v%64) of word v/64 is set for every read start v (PAPER.md:121:
+// k-mers never span two reads)
+__global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t n_reads, uint64_t* rs) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n_reads;
        r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t a = read_start[r], b = read_start[r + 1];
-    if (a == b) continue;  // empty read owns no position
-    for (uint64_t t = (a + kSTile - 1) / kSTile; t * kSTile < b && t < n_tiles; ++t) tile_first[t] = r;
+    const uint64_t v = read_start[r];
+    if (v < read_start[r + 1]) atomicOr(reinterpret_cast<unsigned long long*>(rs + (v >> 6)), 1ull << (63 - (v & 63)));
   }
 }
 
 __global__ void __launch_bounds__(kThreads, 5)
-supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_t n_tiles, int hist_smem) {
+supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n_tiles, int hist_smem) {
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
   __shared__ uint32_t s_rs[kBitWords];   // read-start bits
@@ -127,8 +131,9 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
   const uint32_t k = a.k, m = a.m, B = a.n_bins;
   const uint32_t w = k - m + 1;
   const uint32_t n_keys = kSTile + k - m;  // m-mers needed by the tile's windows
-  const uint32_t n_bits = kSTile + k;      // staged base positions
   const uint64_t n_code_words = (a.n_bases + 31) / 32, n_mask_words = (a.n_bases + 63) / 64;
+  // rs_bits has n_mask_words + 2 words (the end marker read_start[n_reads] may
+  // sit past the N-mask's last word); words past either end stage as 0
   const int nh = a.bin_words ? 3 : 2;
   const uint32_t mmask = (uint32_t)((1ull << (2 * m)) - 1);
   const uint64_t end_p = a.n_bases >= k ? a.n_bases - k + 1 : 0;  // windows start below this
@@ -138,30 +143,42 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
   if (hist_smem)
     for (uint32_t b = tid; b < nh * B; b += kThreads) s_hist[b] = 0;
   uint64_t my_windows = 0;
+  // 1. staging: thread t owns one u64 of a tile — code word t, or N word
+  //    t - kCodeWords, or read-start word t - kCodeWords - kBitWords64
+  auto stage_load = [&](uint64_t tile) -> uint64_t {
+    if (tile >= n_tiles) return 0ull;
+    const uint64_t p0 = tile * kSTile;
+    if (tid < (uint32_t)kCodeWords) {
+      const uint64_t i = (p0 >> 5) + tid;
+      return i < n_code_words ? __ldg(a.codes + i) : 0ull;
+    }
+    if (tid < (uint32_t)(kCodeWords + 2 * kBitWords64)) {
+      const bool is_n = tid < (uint32_t)(kCodeWords + kBitWords64);
+      const uint64_t i = (p0 >> 6) + tid - kCodeWords - (is_n ? 0 : kBitWords64);
+      const uint64_t* src = is_n ? a.nmask : rs_bits;
+      return (src && i < n_mask_words + (is_n ? 0 : 2)) ? __ldg(src + i) : 0ull;
+    }
+    return 0ull;
+  };
+  auto stage_store = [&](uint64_t v) {  // bitmaps: u64 MSB-first → u32 LSB-first
+    if (tid < (uint32_t)kCodeWords) {
+      s_codes[tid] = v;
+    } else if (tid < (uint32_t)(kCodeWords + 2 * kBitWords64)) {
+      const bool is_n = tid < (uint32_t)(kCodeWords + kBitWords64);
+      const uint32_t i = tid - kCodeWords - (is_n ? 0 : kBitWords64);
+      uint32_t* dst = is_n ? s_n : s_rs;
+      v = __brevll(v);
+      dst[2 * i] = (uint32_t)v;
+      dst[2 * i + 1] = (uint32_t)(v >> 32);
+    }
+  };
+  uint64_t staged = stage_load(blockIdx.x);
 
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const uint64_t p0 = tile * kSTile;
-    // 1. stage codes and N bits (u64 MSB-first → u32 LSB-first via bit reversal)
-    const uint64_t wb = p0 >> 5;
-    for (uint32_t i = tid; i < (uint32_t)kCodeWords; i += kThreads)
-      s_codes[i] = (wb + i < n_code_words) ? __ldg(a.codes + wb + i) : 0ull;
-    const uint64_t mb = p0 >> 6;
-    for (uint32_t i = tid; i < (uint32_t)(kBitWords / 2); i += kThreads) {
-      uint64_t v = (a.nmask && mb + i < n_mask_words) ? __ldg(a.nmask + mb + i) : 0ull;
-      v = __brevll(v);
-      s_n[2 * i] = (uint32_t)v;
-      s_n[2 * i + 1] = (uint32_t)(v >> 32);
-      s_rs[2 * i] = 0u;
-      s_rs[2 * i + 1] = 0u;
-    }
+    stage_store(staged);
     __syncthreads();
-    // read boundaries inside (p0, p0 + n_bits); read_start[n_reads] marks the end
-    const uint64_t lim = p0 + n_bits;
-    for (uint64_t r = tile_first[tile] + 1 + tid; r <= a.n_reads; r += kThreads) {
-      const uint64_t v = __ldg(a.read_start + r);
-      if (v >= lim) break;
-      if (v > p0) atomicOr(&s_rs[(uint32_t)(v - p0) >> 5], 1u << ((uint32_t)(v - p0) & 31));
-    }
+    staged = stage_load(tile + gridDim.x);  // in flight while this tile is processed
     // 2. rolling strand-symmetric m-mer keys of key block t (kKB keys, exactly
     //    one block per thread), block prefix/suffix minima
     {
@@ -338,13 +355,15 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ tile_first, uint64_
 
 }  // namespace
 
-cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms, cudaStream_t st) {
+cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t st) {
   const uint64_t n_tiles = (a.n_bases + kSTile - 1) / kSTile;
   if (n_tiles == 0) return cudaSuccess;
+  cudaError_t e0 = cudaMemsetAsync(rs_bits, 0, supermer_scratch_words(a.n_bases) * 8, st);
+  if (e0 != cudaSuccess) return e0;
   if (a.n_reads) {
     uint64_t g = (a.n_reads + 255) / 256;
     if (g > (uint64_t)sms * 16) g = (uint64_t)sms * 16;
-    tile_reads_kernel<<<(unsigned)g, 256, 0, st>>>(a.read_start, a.n_reads, n_tiles, tile_first);
+    rs_bits_kernel<<<(unsigned)g, 256, 0, st>>>(a.read_start, a.n_reads, rs_bits);
   }
   const int nh = a.bin_words ? 3 : 2;
   // per-CTA smem histograms only while small: a large one would cap occupancy,
@@ -358,10 +377,10 @@ cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* tile_first, int sms
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sms * per_sm;
   if (grid > n_tiles) grid = n_tiles;
-  supermer_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, tile_first, n_tiles, hist_smem);
+  supermer_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, n_tiles, hist_smem);
   return cudaGetLastError();
 }
 
-uint64_t supermer_tiles(uint64_t n_bases) { return (n_bases + kSTile - 1) / kSTile; }
+uint64_t supermer_scratch_words(uint64_t n_bases) { return (n_bases + 63) / 64 + 2; }
 
 }  // namespace gerbil
