@@ -24,6 +24,9 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
            "-I" + os.path.join(ROOT, "include")] + ARCH
+# tuning experiments only: extra nvcc flags (e.g. -DGERBIL_SM_MINB=4) force a rebuild
+EXTRA = os.environ.get("GERBIL_NVCC_EXTRA", "").split()
+NVFLAGS += EXTRA
 
 GERBIL_CU = ["supermer.cu", "supermer_reads.cu", "shuffle.cu", "count.cu", "compact.cu", "comm.cu", "api.cu"]
 GERBIL_CPP = ["reader.cpp", "output.cpp"]
@@ -56,6 +59,7 @@ def build_gerbil(force: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     hdrs = _headers(CSRC) + [os.path.join(ROOT, "include", "gerbil.h")]
     srcs = [os.path.join(CSRC, f) for f in GERBIL_CU + GERBIL_CPP]
+    force = force or bool(EXTRA)
     if not force and not _stale(LIB_GERBIL, srcs + hdrs):
         return LIB_GERBIL
     jobs = []

@@ -109,7 +109,10 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 5)
+#ifndef GERBIL_SM_MINB
+#define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
+#endif
+__global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n_tiles, int hist_smem) {
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
