@@ -179,6 +179,26 @@ gerbil_status gerbil_count_host_packed(gerbil_ctx* ctx, const uint64_t* codes,
                                        const uint64_t* read_start, uint64_t n_reads,
                                        uint32_t k, uint32_t m, uint32_t min_count);
 
+/* Streaming end-to-end call (steps b→e from HOST buffers to HOST records):
+ * gerbil_count_host_packed, and in the same pass the compaction kernel encodes
+ * every k-mer with count >= min_count as the paper's binary record (App. C,
+ * PAPER.md:512-521; GERBIL_FORMAT_BINARY: 1-byte counter, or 0xFF + 32-bit
+ * big-endian counter when >= 255, then ceil(k/4) bytes, 4 bases per byte MSB
+ * first, zero-padded) and writes it straight into out[0, capacity) over PCIe
+ * while later waves are still being counted — the download overlaps step (d).
+ * Record order is unspecified. out must be page-locked host memory
+ * (cudaHostAlloc / cudaHostRegister) — GERBIL_E_USAGE otherwise — and is
+ * owned by the caller. *n_bytes = size of the complete encoding. If capacity
+ * is too small (capacity = 0 and out = NULL is a sizing call), out's contents
+ * are unspecified, *n_bytes holds the size needed and GERBIL_E_USAGE is
+ * returned; the (k-mer, count) results stay on the device either way
+ * (gerbil_fetch / gerbil_encode_results work as after gerbil_count_device). */
+gerbil_status gerbil_count_host_stream(gerbil_ctx* ctx, const uint64_t* codes,
+                                       const uint64_t* nmask,
+                                       const uint64_t* read_start, uint64_t n_reads,
+                                       uint32_t k, uint32_t m, uint32_t min_count,
+                                       uint8_t* out, uint64_t capacity, uint64_t* n_bytes);
+
 /* Host reader alone (step a): parse FASTA/FASTQ and pack. Two-call pattern:
  * with codes == NULL, returns the sizes (n_bases, n_reads) only. Buffers:
  * codes[ceil(n_bases/32)], nmask[ceil(n_bases/64)], read_start[n_reads+1]. */

@@ -90,6 +90,14 @@ struct TimedEvent {
   cudaEvent_t a, b;
 };
 
+// A host batch uploaded in chunks (gerbil_count_host_packed): after ev[c],
+// bases [0, base_end[c]) and read_start[0, read_end[c]] are resident.
+struct UploadPlan {
+  uint64_t n_bases = 0;
+  std::vector<uint64_t> base_end, read_end;
+  std::vector<cudaEvent_t> ev;
+};
+
 struct Wave {
   uint64_t d0, d1;   // descriptor range (bin-ordered)
   uint64_t windows;
@@ -104,7 +112,9 @@ struct gerbil_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t lane_stream = nullptr;             // second wave lane (steps d+e)
+  cudaStream_t pcie_stream = nullptr;             // record copies to the host (streaming call)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  std::vector<cudaEvent_t> wave_ev;               // "wave w compacted" (streaming call)
   bool poisoned = false;
   std::string err;
   double rho = 0.5;
@@ -117,6 +127,7 @@ struct gerbil_ctx {
   DevBuf hist;  // [3][B] windows, super-mers, payload words (ull)
   DevBuf hist_all, cursor, cursor2, seg_base;
   DevBuf table, ovf, out_keys, out_counts, wave_distinct;
+  DevBuf rec_stage, rec_meta;  // streaming call: per-lane record staging; counters/snapshots/offsets
   DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
   Counters* h_counters = nullptr;  // pinned
   // results
@@ -129,6 +140,13 @@ struct gerbil_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   uint32_t n_launch[K_NKIND] = {0};
+  // streaming record sink of the current call (gerbil_count_host_stream)
+  uint8_t* rec_out = nullptr;
+  uint64_t rec_cap = 0, rec_bytes = 0;
+  unsigned long long* h_snap = nullptr;  // pinned: per-wave record byte counters (streaming call)
+  size_t h_snap_n = 0;
+  const UploadPlan* upload = nullptr;     // chunked upload of the current call, or null
+  std::vector<cudaEvent_t> chunk_ev;
 };
 
 namespace {
@@ -223,6 +241,16 @@ double wall_ms() {
       .count();
 }
 
+// GERBIL_TRACE=1: host wall-clock milestones of a call on stderr (diagnostics)
+void trace(const char* what) {
+  static const bool on = getenv("GERBIL_TRACE") && *getenv("GERBIL_TRACE") == '1';
+  static double t0 = 0;
+  if (!on) return;
+  const double t = wall_ms();
+  if (strcmp(what, "call") == 0) t0 = t;
+  fprintf(stderr, "[gerbil] %9.3f ms  %s\n", t - t0, what);
+}
+
 // ---------------------------------------------------------------------------
 // Steps (d)+(e) over the bin-ordered descriptors of this rank.
 gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
@@ -301,10 +329,74 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ca.out_n = &dc->out_n;
     ca.sum_counts = &dc->sum_counts;
     ca.distinct = &dc->distinct;
+    // Streaming call: each lane's compactions append App. C records to the
+    // lane's HBM staging area; after compact(w) the lane's byte counter is
+    // copied to pinned host memory (h_snap[w]) and an event marks wave w.
+    // Once every wave is launched, this thread waits for the waves in order
+    // and has the copy engine move [end of the lane's previous wave,
+    // h_snap[w]) of the staging area to the caller's buffer — DMA behind the
+    // counting, no SMs taken from the count kernels. rec_meta: 2 lane counters.
+    const bool streaming = ctx->rec_out != nullptr;
+    const bool two = lanes > 1 && waves.size() > 1;
+    unsigned long long* lane_ctr = nullptr;
+    uint64_t lane_stage_off[2] = {0, 0}, lane_cap[2] = {0, 0};
+    struct Pending {
+      int lane;
+      size_t wi;
+    };
+    std::vector<Pending> pending;
+    uint64_t lane_done[2] = {0, 0}, host_off = 0;
+    if (streaming) {
+      const uint64_t rec_max = 5 + (k + 3) / 4;
+      uint64_t lb[2] = {0, 0};
+      for (size_t w = 0; w < waves.size(); ++w)
+        lb[two ? (w & 1) : 0] += std::min<uint64_t>(waves[w].nb * kSlotsPerBucket, waves[w].windows) * rec_max;
+      lb[0] += ovf_cap * rec_max;
+      lane_stage_off[1] = (lb[0] + 64 + 255) & ~255ull;
+      lane_cap[0] = lb[0];
+      lane_cap[1] = lb[1];
+      CK(ctx->rec_stage.ensure(lane_stage_off[1] + lb[1] + 64));
+      CK(ctx->rec_meta.ensure(2 * 8));
+      CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+      lane_ctr = ctx->rec_meta.as<unsigned long long>();
+      if (ctx->h_snap_n < nw + 1) {
+        if (ctx->h_snap) cudaFreeHost(ctx->h_snap);
+        ctx->h_snap = nullptr;
+        ctx->h_snap_n = 0;
+        CK(cudaMallocHost((void**)&ctx->h_snap, (nw + 1) * 8));
+        ctx->h_snap_n = nw + 1;
+      }
+      while (ctx->wave_ev.size() < nw + 1) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        ctx->wave_ev.push_back(ev);
+      }
+    }
+    // after compact(wi) on st: snapshot lane L's byte counter, mark the wave
+    auto stream_wave = [&](int L, size_t wi, cudaStream_t st) -> gerbil_status {
+      CK(cudaMemcpyAsync(ctx->h_snap + wi, lane_ctr + L, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(ctx->wave_ev[wi], st));
+      pending.push_back({L, wi});
+      return GERBIL_OK;
+    };
+    // wait for each marked wave in order and DMA its records to the caller
+    auto drain_copies = [&]() -> gerbil_status {
+      for (const Pending& pw : pending) {
+        CK(cudaEventSynchronize(ctx->wave_ev[pw.wi]));
+        const uint64_t end = ctx->h_snap[pw.wi], start = lane_done[pw.lane], len = end - start;
+        if (len && host_off + len <= ctx->rec_cap)
+          CK(cudaMemcpyAsync(ctx->rec_out + host_off, ctx->rec_stage.as<uint8_t>() + lane_stage_off[pw.lane] + start,
+                             len, cudaMemcpyDeviceToHost, ctx->pcie_stream));
+        lane_done[pw.lane] = end;
+        host_off += len;
+      }
+      pending.clear();
+      return GERBIL_OK;
+    };
+    trace("waves planned, buffers ready");
     {
       // with two lanes the per-launch events would overlap: one span timer
       // covers steps (d)+(e) and is reported as ms_count (ms_compact = 0)
-      const bool two = lanes > 1 && waves.size() > 1;
       Timer span(ctx, K_COUNT, ctx->stream, two, 0);
       if (two) {
         CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
@@ -325,16 +417,24 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
         ca.table = t.table;
         ca.nb = waves[w].nb;
         ca.wave_distinct = ctx->wave_distinct.as<unsigned long long>() + w;
+        if (streaming) {
+          ca.rec_out = ctx->rec_stage.as<uint8_t>() + lane_stage_off[lane];
+          ca.rec_cap = lane_cap[lane];
+          ca.rec_n = lane_ctr + lane;
+        }
         {
           Timer tm(ctx, K_COMPACT, st, !two);
           CK(launch_compact(ca, ctx->sms, st));
         }
+        if (streaming) CKS(stream_wave(lane, w, st));
       }
       if (two) {
         CK(cudaEventRecord(ctx->join_ev, ctx->lane_stream));
         CK(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
       }
     }
+    trace("waves launched");
+    if (streaming) CKS(drain_copies());
     CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
     std::vector<unsigned long long> wd(waves.size());
     if (!waves.empty())
@@ -364,8 +464,14 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ctx->stats.probe_more = hc.probe[1];
     ctx->stats.probe_max = hc.probe[2];
     const uint64_t ovf_n = hc.ovf_n;
+    trace("waves done (synced)");
     if (ovf_n > ovf_cap) {
-      // emergency area exhausted: redo the waves with larger tables
+      // emergency area exhausted: redo the waves with larger tables (after
+      // this attempt's record copies, which write the same host buffer)
+      if (streaming) {
+        CK(cudaStreamSynchronize(ctx->pcie_stream));
+        lane_done[0] = lane_done[1] = host_off = 0;
+      }
       ctx->rho = std::min(1.0, std::max(2.0 * rho, 1.25 * observed + 0.02));
       if (attempt > 8) return fail(ctx, GERBIL_E_INTERNAL, "table sizing did not converge");
       continue;
@@ -392,9 +498,18 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
       c2.table = t2.table;
       c2.nb = nb2;
       c2.wave_distinct = nullptr;
+      if (streaming) {  // lane 0's staging area has room for the emergency pass
+        c2.rec_out = ctx->rec_stage.as<uint8_t>();
+        c2.rec_cap = lane_cap[0];
+        c2.rec_n = lane_ctr;
+      }
       {
         Timer tm(ctx, K_OVERFLOW);
         CK(launch_compact(c2, ctx->sms, ctx->stream));
+      }
+      if (streaming) {
+        CKS(stream_wave(0, nw, ctx->stream));
+        CKS(drain_copies());
       }
       CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
@@ -405,6 +520,11 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     // ratio adaptation for the next call ("we dynamically adjust the ratio")
     if (observed > 0) ctx->rho = std::min(1.0, std::max(observed * 1.15 + 0.01, 0.02));
     ctx->n_out = hc.out_n;
+    if (streaming) {  // wait for the last record copies
+      CK(cudaStreamSynchronize(ctx->pcie_stream));
+      ctx->rec_bytes = host_off;
+      trace("record copies done (synced)");
+    }
     ctx->stats.kept = hc.out_n;
     ctx->stats.distinct = hc.distinct;
     ctx->stats.count_sum = hc.sum_counts;
@@ -446,9 +566,39 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     a.bin_windows = h;
     a.bin_supermers = h + B;
     a.bin_words = ctx->comm ? h + 2 * B : nullptr;
+    const UploadPlan* up = ctx->upload;
     if (use_reads_kernel(k, m, n_bases, n_reads)) {
+      if (up)
+        for (cudaEvent_t ev : up->ev) CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
       Timer tm(ctx, K_SUPERMER);
       CK(launch_supermer_reads(a, &dc->read_work, ctx->sms, ctx->stream));
+    } else if (up) {
+      // chunked upload: mark each chunk's reads and run the tiles it completes
+      // as soon as it lands, so step (b) runs behind the H2D copies
+      CK(ctx->rs_bits.ensure(supermer_scratch_words(n_bases) * 8));
+      uint64_t* rs = ctx->rs_bits.as<uint64_t>();
+      const uint64_t n_tiles = supermer_tile_count(n_bases), reach = supermer_tile_reach();
+      Timer tm(ctx, K_SUPERMER, nullptr, true, 0);
+      CK(supermer_prepare(a, rs, ctx->stream));
+      uint64_t r0 = 0, t0 = 0;
+      for (size_t c = 0; c < up->ev.size(); ++c) {
+        CK(cudaStreamWaitEvent(ctx->stream, up->ev[c], 0));
+        const uint64_t r1 = up->read_end[c];
+        if (r1 > r0) {
+          CK(supermer_mark_reads(a, rs, r0, r1, ctx->sms, ctx->stream));
+          ctx->n_launch[K_SUPERMER]++;
+        }
+        r0 = std::max(r0, r1);
+        const bool last = c + 1 == up->ev.size();
+        const uint64_t be = up->base_end[c];
+        uint64_t t1 = last ? n_tiles : (be >= reach ? std::min(n_tiles, (be - reach) / 1024 + 1) : 0);
+        t1 = std::max(t1, t0);
+        if (t1 > t0) {
+          CK(supermer_run_tiles(a, rs, t0, t1, ctx->sms, ctx->stream));
+          ctx->n_launch[K_SUPERMER]++;
+        }
+        t0 = t1;
+      }
     } else {
       CK(ctx->rs_bits.ensure(supermer_scratch_words(n_bases) * 8));
       Timer tm(ctx, K_SUPERMER, nullptr, true, n_reads ? 2u : 1u);  // rs_bits_kernel + supermer_kernel
@@ -463,21 +613,28 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
   return fail(ctx, GERBIL_E_INTERNAL, "super-mer buffer sizing did not converge");
 }
 
-gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
-                                const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
-                                uint32_t min_count) {
-  const double t0 = wall_ms();
-  ctx->have_result = false;
-  ctx->n_out = 0;
+// per-call timing/launch bookkeeping reset (before any timed work of the call)
+void begin_call(gerbil_ctx* ctx) {
   ctx->evs.clear();
   ctx->ev_used = 0;
   for (auto& v : ctx->n_launch) v = 0;
+}
+
+gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                uint32_t min_count, bool fresh = true) {
+  const double t0 = wall_ms();
+  ctx->have_result = false;
+  ctx->n_out = 0;
+  if (fresh) begin_call(ctx);
   memset(&ctx->stats, 0, sizeof ctx->stats);
   const uint32_t W = key_words(k);
   ctx->W = W;
   ctx->k = k;
   uint64_t n_bases = 0;
-  if (n_reads > 0) {
+  if (ctx->upload) {
+    n_bases = ctx->upload->n_bases;  // host batch: known without waiting for the upload
+  } else if (n_reads > 0) {
     CK(cudaMemcpyAsync(&ctx->h_counters->probe[3], rstart + n_reads, 8, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -497,7 +654,9 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
 
   // (b)
   uint64_t n_sm = 0;
+  trace("supermer issue");
   CKS(run_supermer(ctx, codes, nmask, rstart, n_reads, n_bases, k, m, B, false, n_sm));
+  trace("supermer done (synced)");
   const uint64_t local_windows = ctx->h_counters->n_windows;
   ctx->stats.supermers = n_sm;
   ctx->stats.valid_windows = local_windows;
@@ -669,6 +828,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   }
 
   // (d) + (e)
+  trace("scatter issued");
   CKS(count_waves(ctx, stream_codes, ctx->desc_sorted.as<uint64_t>(), bin_off, bin_win, owned, k,
                   min_count, owned_windows));
   // Σ-count invariant: every valid window counted exactly once
@@ -684,6 +844,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
       cudaEventElapsedTime(&f, e.a, e.b);
       ms[e.kind] += f;
     }
+    ctx->stats.ms_h2d = ms[K_H2D];
     ctx->stats.ms_supermer = ms[K_SUPERMER];
     ctx->stats.ms_shuffle = ms[K_SHUFFLE];
     ctx->stats.ms_count = ms[K_COUNT];
@@ -754,6 +915,7 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->lane_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pcie_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMallocHost((void**)&ctx->h_counters, sizeof(Counters));
   if (e != cudaSuccess) {
     delete ctx;
@@ -790,6 +952,13 @@ void gerbil_finalize(gerbil_ctx* ctx) {
     cudaStreamSynchronize(ctx->lane_stream);
     cudaStreamDestroy(ctx->lane_stream);
   }
+  if (ctx->pcie_stream) {
+    cudaStreamSynchronize(ctx->pcie_stream);
+    cudaStreamDestroy(ctx->pcie_stream);
+  }
+  for (auto ev : ctx->wave_ev) cudaEventDestroy(ev);
+  for (auto ev : ctx->chunk_ev) cudaEventDestroy(ev);
+  if (ctx->h_snap) cudaFreeHost(ctx->h_snap);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -827,15 +996,88 @@ gerbil_status gerbil_count_host_packed(gerbil_ctx* ctx, const uint64_t* codes, c
   CK(ctx->in_codes.ensure(ncw * 8));
   CK(ctx->in_nmask.ensure(nmw * 8));
   CK(ctx->in_rstart.ensure((n_reads + 1) * 8));
-  {
-    Timer tm(ctx, K_H2D);
-    CK(cudaMemcpyAsync(ctx->in_codes.p, codes, ((nb + 31) / 32) * 8, cudaMemcpyHostToDevice, ctx->stream));
-    if (nmask)
-      CK(cudaMemcpyAsync(ctx->in_nmask.p, nmask, ((nb + 63) / 64) * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->in_rstart.p, rstart, (n_reads + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  trace("call");
+  begin_call(ctx);
+  // Upload in chunks on the copy stream (64-base-word boundaries); step (b)
+  // consumes each chunk as it lands (run_supermer). GERBIL_UPLOAD_CHUNKS
+  // overrides the count (tests force several chunks on small inputs).
+  uint64_t nch = std::min<uint64_t>(16, std::max<uint64_t>(1, nb >> 26));
+  if (const char* e = getenv("GERBIL_UPLOAD_CHUNKS"))
+    if (*e) nch = std::max<uint64_t>(1, std::min<uint64_t>(strtoull(e, nullptr, 10), std::max<uint64_t>(nmw, 1)));
+  UploadPlan plan;
+  plan.n_bases = nb;
+  while (ctx->chunk_ev.size() < nch) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->chunk_ev.push_back(ev);
   }
-  return count_device_impl(ctx, ctx->in_codes.as<uint64_t>(), nmask ? ctx->in_nmask.as<uint64_t>() : nullptr,
-                           ctx->in_rstart.as<uint64_t>(), n_reads, k, m, min_count);
+  // the copies may start only after earlier work on the main stream (a
+  // previous call still reading these buffers)
+  CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->pcie_stream, ctx->fork_ev, 0));
+  {
+    Timer tm(ctx, K_H2D, ctx->pcie_stream, true, 0);
+    uint64_t w0 = 0, r0 = 0;
+    for (uint64_t c = 0; c < nch; ++c) {
+      const bool last = c + 1 == nch;
+      const uint64_t w1 = last ? nmw : (c + 1) * nmw / nch;  // N-mask words [w0, w1)
+      const uint64_t be = std::min<uint64_t>(w1 * 64, nb);
+      const uint64_t cw0 = std::min<uint64_t>(2 * w0, (nb + 31) / 32), cw1 = std::min<uint64_t>(2 * w1, (nb + 31) / 32);
+      const uint64_t r1 = last ? n_reads : (uint64_t)(std::lower_bound(rstart, rstart + n_reads, be) - rstart);
+      if (cw1 > cw0)
+        CK(cudaMemcpyAsync(ctx->in_codes.as<uint64_t>() + cw0, codes + cw0, (cw1 - cw0) * 8,
+                           cudaMemcpyHostToDevice, ctx->pcie_stream));
+      if (nmask && nb > 0 && w1 > w0)
+        CK(cudaMemcpyAsync(ctx->in_nmask.as<uint64_t>() + w0, nmask + w0, (w1 - w0) * 8, cudaMemcpyHostToDevice,
+                           ctx->pcie_stream));
+      const uint64_t rs0 = c == 0 ? 0 : r0 + 1;  // read_start[r0] came with the previous chunk
+      if (r1 + 1 > rs0)
+        CK(cudaMemcpyAsync(ctx->in_rstart.as<uint64_t>() + rs0, rstart + rs0, (r1 + 1 - rs0) * 8,
+                           cudaMemcpyHostToDevice, ctx->pcie_stream));
+      CK(cudaEventRecord(ctx->chunk_ev[c], ctx->pcie_stream));
+      plan.base_end.push_back(be);
+      plan.read_end.push_back(r1);
+      plan.ev.push_back(ctx->chunk_ev[c]);
+      w0 = w1;
+      r0 = r1;
+    }
+  }
+  ctx->upload = &plan;
+  const gerbil_status st =
+      count_device_impl(ctx, ctx->in_codes.as<uint64_t>(), nmask ? ctx->in_nmask.as<uint64_t>() : nullptr,
+                        ctx->in_rstart.as<uint64_t>(), n_reads, k, m, min_count, false);
+  ctx->upload = nullptr;
+  // every chunk event has been waited on by the main stream unless the call
+  // failed early; make sure no copy outlives the call
+  if (st != GERBIL_OK) cudaStreamSynchronize(ctx->pcie_stream);
+  return st;
+}
+
+gerbil_status gerbil_count_host_stream(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                                       const uint64_t* rstart, uint64_t n_reads, uint32_t k, uint32_t m,
+                                       uint32_t min_count, uint8_t* out, uint64_t capacity, uint64_t* n_bytes) {
+  if (!ctx || !n_bytes) return GERBIL_E_USAGE;
+  *n_bytes = 0;
+  if (capacity > 0) {
+    if (!out) return fail(ctx, GERBIL_E_USAGE, "null output buffer");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, out) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return fail(ctx, GERBIL_E_USAGE, "output buffer must be page-locked host memory (cudaHostAlloc/Register)");
+    }
+  }
+  // a dummy sink keeps the encoder on when capacity == 0 (sizing call: nothing is copied)
+  ctx->rec_out = capacity > 0 ? out : reinterpret_cast<uint8_t*>(1);
+  ctx->rec_cap = capacity;
+  const gerbil_status st = gerbil_count_host_packed(ctx, codes, nmask, rstart, n_reads, k, m, min_count);
+  ctx->rec_out = nullptr;
+  ctx->rec_cap = 0;
+  if (st != GERBIL_OK) return st;
+  *n_bytes = ctx->rec_bytes;
+  if (ctx->rec_bytes > capacity)
+    return fail(ctx, GERBIL_E_USAGE, "output capacity " + std::to_string(capacity) + " < " +
+                                         std::to_string(ctx->rec_bytes) + " record bytes");
+  return GERBIL_OK;
 }
 
 gerbil_status gerbil_pack_reads(const gerbil_reads* reads, int32_t threads, uint64_t* codes,

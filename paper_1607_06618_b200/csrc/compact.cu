@@ -11,6 +11,16 @@
 // result layout (include/gerbil.h). The same pass sums every count (Σ-count
 // invariant), counts distinct keys, and clears the slots it
 // read, so the L2-resident table buffer is clean for the next wave.
+//
+// Optionally (streaming e2e path) the same pass encodes every kept k-mer as
+// the paper's binary record (App. C: 1-byte counter, or
+// 0xFF + 32-bit big-endian counter when >= 255, then ceil(k/4) bytes of 2-bit
+// bases MSB-first): records are placed in shared memory by the same block
+// scan (at the destination's 16-byte phase), one atomic per CTA iteration
+// reserves their byte range in the lane's HBM staging buffer, and the CTA
+// writes it with aligned 16-byte stores; the host then has the copy engine
+// move each wave's records to page-locked host memory behind the counting of
+// the next waves (api.cu, gerbil_count_host_stream).
 #include "common.cuh"
 #include "kernels.h"
 #include "table.cuh"
@@ -23,9 +33,48 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPer = 4;
 
+__device__ __forceinline__ uint32_t record_bytes(uint32_t kb, uint32_t cnt) { return (cnt < 255 ? 1u : 5u) + kb; }
+
+// App. C record of (key, cnt) at s[o..): counter, then the key's big-endian bytes
+__device__ __forceinline__ void put_record(uint8_t* s, uint32_t o, const uint64_t* key, uint32_t kb, uint32_t cnt) {
+  if (cnt < 255) {
+    s[o++] = (uint8_t)cnt;
+  } else {
+    s[o++] = 0xFF;
+    s[o++] = (uint8_t)(cnt >> 24);
+    s[o++] = (uint8_t)(cnt >> 16);
+    s[o++] = (uint8_t)(cnt >> 8);
+    s[o++] = (uint8_t)cnt;
+  }
+  for (uint32_t b = 0; b < kb; ++b) s[o++] = (uint8_t)(key[b >> 3] >> (56 - 8 * (b & 7)));
+}
+
+// all threads: copy the staged range to out[dst0, dst0 + tot), unless it passes
+// cap. The records were staged at smem offset dst0 % 16, so smem and the
+// destination share their alignment: whole 16-byte blocks move with one vector
+// load/store each, the (at most two) partial edge blocks byte by byte.
+__device__ __forceinline__ void flush_records(const uint8_t* s, uint32_t tot, uint64_t dst0, uint8_t* out,
+                                              uint64_t cap) {
+  if (tot == 0 || dst0 + tot > cap) return;
+  const uint32_t a0 = (uint32_t)(dst0 & 15), end = a0 + tot;
+  uint8_t* base = out + (dst0 - a0);
+  const uint32_t nblk = (end + 15) >> 4;
+  for (uint32_t b = threadIdx.x; b < nblk; b += blockDim.x) {
+    const uint32_t lo = b << 4, hi = lo + 16;
+    if (lo >= a0 && hi <= end) {
+      *reinterpret_cast<uint4*>(base + lo) = *reinterpret_cast<const uint4*>(s + lo);
+    } else {
+      for (uint32_t i = max(lo, a0); i < min(hi, end); ++i) base[i] = s[i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
-  __shared__ uint32_t s_cnt[kWarps * kPer];
-  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_cnt[kWarps * kPer], s_big[kWarps * kPer];
+  __shared__ unsigned long long s_base, s_rbase;
+  __shared__ uint32_t s_rtot;
+  extern __shared__ __align__(16) uint8_t s_rec[];  // [16 + kThreads * kPer * (5 + kb)] when a.rec_out
+  const uint32_t kb = (a.k + 3) / 4;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint32_t W = key_words(a.k);
   const bool inl = table_inline(a.k);
@@ -35,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
   for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kPer; base < n_slots;
        base += (uint64_t)gridDim.x * kThreads * kPer) {
     uint64_t c0[kPer], c1[kPer];
-    uint32_t cnt[kPer], rank[kPer];
+    uint32_t cnt[kPer], rank[kPer], brank[kPer];
     bool keep[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -58,17 +107,28 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
       keep[j] = c0[j] != 0 && cnt[j] >= a.min_count;
       const uint32_t m = __ballot_sync(0xffffffffu, keep[j]);
       rank[j] = __popc(m & ((1u << lane) - 1u));
-      if (lane == 0) s_cnt[j * kWarps + warp] = __popc(m);
+      const uint32_t mb = __ballot_sync(0xffffffffu, keep[j] && cnt[j] >= 255);
+      brank[j] = __popc(mb & ((1u << lane) - 1u));
+      if (lane == 0) {
+        s_cnt[j * kWarps + warp] = __popc(m);
+        s_big[j * kWarps + warp] = __popc(mb);
+      }
     }
     __syncthreads();
     if (tid == 0) {
-      uint32_t run = 0;
+      uint32_t run = 0, runb = 0;
       for (int i = 0; i < kWarps * kPer; ++i) {
-        const uint32_t v = s_cnt[i];
+        const uint32_t v = s_cnt[i], vb = s_big[i];
         s_cnt[i] = run;
+        s_big[i] = runb;
         run += v;
+        runb += vb;
       }
       s_base = run ? atomicAdd(a.out_n, (unsigned long long)run) : 0ull;
+      if (a.rec_out) {
+        s_rtot = run * (1 + kb) + 4 * runb;
+        s_rbase = s_rtot ? atomicAdd(a.rec_n, (unsigned long long)s_rtot) : 0ull;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -90,6 +150,10 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
           from_chunks(ch, WP, key, W);
           for (uint32_t w = 0; w < W; ++w) a.out_keys[idx * W + w] = key[w];
           a.out_counts[idx] = cnt[j];
+          if (a.rec_out) {
+            const uint32_t r = s_cnt[j * kWarps + warp] + rank[j], rb = s_big[j * kWarps + warp] + brank[j];
+            put_record(s_rec, (uint32_t)(s_rbase & 15) + r * (1 + kb) + 4 * rb, key, kb, cnt[j]);
+          }
         }
       }
       my_sum += cnt[j];
@@ -105,6 +169,10 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
       }
     }
     __syncthreads();
+    if (a.rec_out) {
+      flush_records(s_rec, s_rtot, s_rbase, a.rec_out, a.rec_cap);
+      __syncthreads();
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -123,10 +191,33 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
 // store covers whole 32-byte sectors across the warp.
 constexpr int kPerI = 8;
 
+// one warp: exclusive scan in place of c[0..n) (n <= 64, two entries per lane); returns the total
+__device__ __forceinline__ uint32_t excl_scan64(uint32_t* c, uint32_t n) {
+  const uint32_t lane = lane_id();
+  const uint32_t x0 = lane < n ? c[lane] : 0u;
+  const uint32_t x1 = lane + 32 < n ? c[lane + 32] : 0u;
+  uint32_t i0 = x0, i1 = x1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o);
+    if (lane >= (uint32_t)o) {
+      i0 += t0;
+      i1 += t1;
+    }
+  }
+  const uint32_t tot0 = __shfl_sync(0xffffffffu, i0, 31);
+  if (lane < n) c[lane] = i0 - x0;
+  if (lane + 32 < n) c[lane + 32] = tot0 + i1 - x1;
+  return tot0 + __shfl_sync(0xffffffffu, i1, 31);
+}
+
 template <int W, bool TWO>
 __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a) {
-  __shared__ uint32_t s_cnt[kWarps * kPerI];
-  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_cnt[kWarps * kPerI], s_big[kWarps * kPerI];
+  __shared__ unsigned long long s_base, s_rbase;
+  __shared__ uint32_t s_rtot;
+  extern __shared__ __align__(16) uint8_t s_rec[];  // [16 + kThreads * kPerI * (5 + kb)] when a.rec_out
+  const uint32_t kb = (a.k + 3) / 4;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint64_t n_slots = a.nb * kSlotsPerBucket;
   ulonglong2* slots = reinterpret_cast<ulonglong2*>(a.table);
@@ -134,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
   for (uint64_t base = (uint64_t)blockIdx.x * kThreads * kPerI; base < n_slots;
        base += (uint64_t)gridDim.x * kThreads * kPerI) {
     ulonglong2 v[kPerI];
-    uint32_t rank[kPerI];
+    uint32_t rank[kPerI], brank[kPerI];
     uint32_t keepm = 0;
 #pragma unroll
     for (int j = 0; j < kPerI; ++j) {
@@ -144,23 +235,24 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
       keepm |= (uint32_t)keep << j;
       const uint32_t m = __ballot_sync(0xffffffffu, keep);
       rank[j] = __popc(m & ((1u << lane) - 1u));
-      if (lane == 0) s_cnt[j * kWarps + warp] = __popc(m);
+      const uint32_t mb = __ballot_sync(0xffffffffu, keep && (uint32_t)v[j].y >= 255);
+      brank[j] = __popc(mb & ((1u << lane) - 1u));
+      if (lane == 0) {
+        s_cnt[j * kWarps + warp] = __popc(m);
+        s_big[j * kWarps + warp] = __popc(mb);
+      }
     }
     __syncthreads();
-    if (tid < 32) {  // exclusive scan of the kWarps*kPerI counts (<= 64) by one warp
-      const uint32_t x0 = tid < kWarps * kPerI ? s_cnt[tid] : 0u;
-      const uint32_t x1 = tid + 32 < kWarps * kPerI ? s_cnt[tid + 32] : 0u;
-      uint32_t i0 = x0, i1 = x1;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o);
-        if (lane >= (uint32_t)o) { i0 += t0; i1 += t1; }
+    if (tid < 32) {  // exclusive scans of the kWarps*kPerI (<= 64) keep / big counts by one warp
+      const uint32_t run = excl_scan64(s_cnt, kWarps * kPerI);
+      const uint32_t runb = excl_scan64(s_big, kWarps * kPerI);
+      if (tid == 0) {
+        s_base = run ? atomicAdd(a.out_n, (unsigned long long)run) : 0ull;
+        if (a.rec_out) {
+          s_rtot = run * (1 + kb) + 4 * runb;
+          s_rbase = s_rtot ? atomicAdd(a.rec_n, (unsigned long long)s_rtot) : 0ull;
+        }
       }
-      const uint32_t tot0 = __shfl_sync(0xffffffffu, i0, 31);
-      if (tid < kWarps * kPerI) s_cnt[tid] = i0 - x0;
-      if (tid + 32 < kWarps * kPerI) s_cnt[tid + 32] = tot0 + i1 - x1;
-      const uint32_t run = tot0 + __shfl_sync(0xffffffffu, i1, 31);
-      if (tid == 0) s_base = run ? atomicAdd(a.out_n, (unsigned long long)run) : 0ull;
     }
     __syncthreads();
 #pragma unroll
@@ -176,6 +268,10 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
           if (W == 2) reinterpret_cast<ulonglong2*>(a.out_keys)[idx] = make_ulonglong2(key[0], key[1]);
           else a.out_keys[idx] = key[0];
           a.out_counts[idx] = cnt;
+          if (a.rec_out) {
+            const uint32_t r = s_cnt[j * kWarps + warp] + rank[j], rb = s_big[j * kWarps + warp] + brank[j];
+            put_record(s_rec, (uint32_t)(s_rbase & 15) + r * (1 + kb) + 4 * rb, key, kb, cnt);
+          }
         }
       }
       my_sum += cnt;
@@ -183,6 +279,10 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
       slots[slot] = make_ulonglong2(0ull, 0ull);
     }
     __syncthreads();
+    if (a.rec_out) {
+      flush_records(s_rec, s_rtot, s_rbase, a.rec_out, a.rec_cap);
+      __syncthreads();
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -201,17 +301,27 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
 cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t st) {
   const uint64_t n_slots = a.nb * kSlotsPerBucket;
   if (n_slots == 0) return cudaSuccess;
+  const uint32_t rec_max = 5 + (a.k + 3) / 4;  // largest App. C record
   if (table_inline(a.k)) {
     uint64_t grid = (n_slots + kThreads * kPerI - 1) / (kThreads * kPerI);
     if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
-    if (a.k <= 31) compact_inline_kernel<1, false><<<(unsigned)grid, kThreads, 0, st>>>(a);
-    else if (a.k == 32) compact_inline_kernel<1, true><<<(unsigned)grid, kThreads, 0, st>>>(a);
-    else compact_inline_kernel<2, true><<<(unsigned)grid, kThreads, 0, st>>>(a);
-    return cudaGetLastError();
+    const size_t dyn = a.rec_out ? 16 + (size_t)kThreads * kPerI * rec_max : 0;
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return e;
+      kern<<<(unsigned)grid, kThreads, dyn, st>>>(a);
+      return cudaGetLastError();
+    };
+    if (a.k <= 31) return go(compact_inline_kernel<1, false>);
+    if (a.k == 32) return go(compact_inline_kernel<1, true>);
+    return go(compact_inline_kernel<2, true>);
   }
   uint64_t grid = (n_slots + kThreads * kPer - 1) / (kThreads * kPer);
   if (grid > (uint64_t)sms * 8) grid = (uint64_t)sms * 8;
-  compact_kernel<<<(unsigned)grid, kThreads, 0, st>>>(a);
+  const size_t dyn = a.rec_out ? 16 + (size_t)kThreads * kPer * rec_max : 0;
+  cudaError_t e = cudaFuncSetAttribute(compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  compact_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a);
   return cudaGetLastError();
 }
 

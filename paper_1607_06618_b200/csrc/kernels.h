@@ -32,6 +32,17 @@ cudaError_t launch_supermer_reads(const SupermerArgs& a, unsigned long long* wor
 // rs_bits: scratch of supermer_scratch_words(n_bases) u64 (read-start bitmap).
 cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t s);
 uint64_t supermer_scratch_words(uint64_t n_bases);
+// The same in pieces, for a batch that arrives in chunks: clear the bitmap,
+// mark the starts of reads [r0, r1) (read_start[r1] must be resident), run
+// tiles [t0, t1) (their bases [0, t1*1024 + supermer_tile_reach()) resident,
+// and every read starting below that marked).
+cudaError_t supermer_prepare(const SupermerArgs& a, uint64_t* rs_bits, cudaStream_t s);
+cudaError_t supermer_mark_reads(const SupermerArgs& a, uint64_t* rs_bits, uint64_t r0, uint64_t r1, int sms,
+                                cudaStream_t s);
+cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, uint64_t t0, uint64_t t1, int sms,
+                               cudaStream_t s);
+uint64_t supermer_tile_count(uint64_t n_bases);
+uint64_t supermer_tile_reach();
 
 struct ScatterArgs {
   const uint64_t* desc_in;
@@ -103,8 +114,15 @@ struct CompactArgs {
   unsigned long long* sum_counts;
   unsigned long long* distinct;
   unsigned long long* wave_distinct;  // per-wave slot or nullptr
+  // optional App. C record stream: every kept k-mer is also
+  // encoded into rec_out (page-locked host memory) at a byte range reserved on
+  // *rec_n; nothing is written past rec_cap (rec_n still counts every byte)
+  uint8_t* rec_out;
+  uint64_t rec_cap;
+  unsigned long long* rec_n;
 };
 cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t s);
+
 
 cudaError_t launch_clear_table(unsigned char* table, uint64_t bytes, int sms, cudaStream_t s);
 

@@ -113,7 +113,8 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
 __global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
-supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n_tiles, int hist_smem) {
+supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,
+                int hist_smem) {
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
   __shared__ uint32_t s_rs[kBitWords];   // read-start bits
@@ -149,7 +150,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n
   // 1. staging: thread t owns one u64 of a tile — code word t, or N word
   //    t - kCodeWords, or read-start word t - kCodeWords - kBitWords64
   auto stage_load = [&](uint64_t tile) -> uint64_t {
-    if (tile >= n_tiles) return 0ull;
+    if (tile >= tile_end) return 0ull;
     const uint64_t p0 = tile * kSTile;
     if (tid < (uint32_t)kCodeWords) {
       const uint64_t i = (p0 >> 5) + tid;
@@ -175,9 +176,9 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n
       dst[2 * i + 1] = (uint32_t)(v >> 32);
     }
   };
-  uint64_t staged = stage_load(blockIdx.x);
+  uint64_t staged = stage_load(tile_begin + blockIdx.x);
 
-  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  for (uint64_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
     const uint64_t p0 = tile * kSTile;
     stage_store(staged);
     __syncthreads();
@@ -358,16 +359,22 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t n
 
 }  // namespace
 
-cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t st) {
-  const uint64_t n_tiles = (a.n_bases + kSTile - 1) / kSTile;
-  if (n_tiles == 0) return cudaSuccess;
-  cudaError_t e0 = cudaMemsetAsync(rs_bits, 0, supermer_scratch_words(a.n_bases) * 8, st);
-  if (e0 != cudaSuccess) return e0;
-  if (a.n_reads) {
-    uint64_t g = (a.n_reads + 255) / 256;
-    if (g > (uint64_t)sms * 16) g = (uint64_t)sms * 16;
-    rs_bits_kernel<<<(unsigned)g, 256, 0, st>>>(a.read_start, a.n_reads, rs_bits);
-  }
+cudaError_t supermer_prepare(const SupermerArgs& a, uint64_t* rs_bits, cudaStream_t st) {
+  return cudaMemsetAsync(rs_bits, 0, supermer_scratch_words(a.n_bases) * 8, st);
+}
+
+cudaError_t supermer_mark_reads(const SupermerArgs& a, uint64_t* rs_bits, uint64_t r0, uint64_t r1, int sms,
+                                cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  uint64_t g = (r1 - r0 + 255) / 256;
+  if (g > (uint64_t)sms * 16) g = (uint64_t)sms * 16;
+  rs_bits_kernel<<<(unsigned)g, 256, 0, st>>>(a.read_start + r0, r1 - r0, rs_bits);
+  return cudaGetLastError();
+}
+
+cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, uint64_t t0, uint64_t t1, int sms,
+                               cudaStream_t st) {
+  if (t1 <= t0) return cudaSuccess;
   const int nh = a.bin_words ? 3 : 2;
   // per-CTA smem histograms only while small: a large one would cap occupancy,
   // and spread global REDs are cheap next to this kernel's arithmetic
@@ -379,10 +386,25 @@ cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, c
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, supermer_kernel, kThreads, dyn);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)sms * per_sm;
-  if (grid > n_tiles) grid = n_tiles;
-  supermer_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, n_tiles, hist_smem);
+  if (grid > t1 - t0) grid = t1 - t0;
+  supermer_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, t0, t1, hist_smem);
   return cudaGetLastError();
 }
+
+cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t st) {
+  const uint64_t n_tiles = supermer_tile_count(a.n_bases);
+  if (n_tiles == 0) return cudaSuccess;
+  cudaError_t e = supermer_prepare(a, rs_bits, st);
+  if (e == cudaSuccess) e = supermer_mark_reads(a, rs_bits, 0, a.n_reads, sms, st);
+  if (e == cudaSuccess) e = supermer_run_tiles(a, rs_bits, 0, n_tiles, sms, st);
+  return e;
+}
+
+uint64_t supermer_tile_count(uint64_t n_bases) { return (n_bases + kSTile - 1) / kSTile; }
+
+// a tile is complete once bases [0, t*kSTile + reach) are resident: its staged
+// code words and bitmap words end below that (kernel step 1)
+uint64_t supermer_tile_reach() { return (uint64_t)kCodeWords * 32 + 64; }
 
 uint64_t supermer_scratch_words(uint64_t n_bases) { return (n_bases + 63) / 64 + 2; }
 

@@ -110,6 +110,8 @@ _lib.gerbil_nccl_unique_id.argtypes = [_P, C.c_size_t]
 _lib.gerbil_count.argtypes = [_P, C.POINTER(Reads), C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_count_device.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_count_host_packed.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
+_lib.gerbil_count_host_stream.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _P,
+                                          C.c_uint64, _U64P]
 _lib.gerbil_pack_reads.argtypes = [C.POINTER(Reads), C.c_int32, _P, _P, _P, _U64P, _U64P, C.c_char_p, C.c_size_t]
 _lib.gerbil_fetch.argtypes = [_P, _P, _P, C.c_uint64, _U64P, C.c_int]
 _lib.gerbil_results_device.argtypes = [_P, C.POINTER(_P), C.POINTER(_P), _U64P, C.POINTER(C.c_uint32)]
@@ -122,13 +124,14 @@ _lib.gerbil_write_results.argtypes = [_P, C.c_char_p, C.c_int32, C.c_int]
 _lib.gerbil_debug_supermers.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32,
                                         _P, _P, _P, _P, C.c_uint64, _U64P]
 for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count_device",
-           "gerbil_count_host_packed", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
+           "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
            "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = [
     "gerbil_config_default", "gerbil_init", "gerbil_nccl_unique_id", "gerbil_count",
-    "gerbil_count_device", "gerbil_count_host_packed", "gerbil_pack_reads", "gerbil_fetch",
+    "gerbil_count_device", "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads",
+    "gerbil_fetch",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
     "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
 ]
@@ -278,6 +281,22 @@ class Gerbil:
     def n_results(self) -> int:
         n = C.c_uint64()
         self._check(_lib.gerbil_fetch(self._h, None, None, 0, C.byref(n), 0))
+        return n.value
+
+    def count_host_stream(self, codes, nmask, read_start, n_reads: int, k: int, m: int = 0, min_count: int = 1,
+                          out: np.ndarray | None = None) -> int:
+        """Host batch in, App. C binary records streamed into `out` (a uint8 array in page-locked
+        memory, e.g. a pinned torch tensor's .numpy()); returns the record bytes. Raises GerbilError
+        (status GERBIL_E_USAGE) when `out` is too small — `needed_bytes` on the error holds the size."""
+        n = C.c_uint64(0)
+        cap = 0 if out is None else out.nbytes
+        rc = _lib.gerbil_count_host_stream(self._h, _ptr(codes), _ptr(nmask), _ptr(read_start), n_reads, k, m,
+                                           min_count, _ptr(out) if out is not None else None, cap, C.byref(n))
+        self.k = k
+        if rc != 0:
+            err = GerbilError(rc, _lib.gerbil_last_error(self._h).decode(errors="replace"))
+            err.needed_bytes = n.value
+            raise err
         return n.value
 
     def fetch(self, sorted: bool = True, out_keys: np.ndarray | None = None,
