@@ -71,9 +71,17 @@ typedef enum {
   GERBIL_E_STATE = 7
 } gerbil_status;
 
-/* Minimizer orderings (§3.1). KMC2 is Gerbil's choice
- * (PAPER.md:157); LEX (A<C<G<T) is the ordering of Fig. 1. */
-typedef enum { GERBIL_ORDER_KMC2 = 0, GERBIL_ORDER_LEX = 1 } gerbil_ordering;
+/* Minimizer orderings (§3.1).
+ * KMC2 is Gerbil's choice; LEX (A<C<G<T) is the ordering of
+ * Fig. 1; CGAT (C<G<A<T), ROBERTS (even positions
+ * complemented, then C<A<T<G), RANDOM (a fixed bijection of the m-mers) and
+ * DFP (distance from pivot dfp_pivot in the sampled frequency order; m <= 12)
+ * are the alternatives the paper evaluates. Results never depend on the
+ * ordering; super-mers, bins and the Fig. Minimizer metrics do. */
+typedef enum {
+  GERBIL_ORDER_KMC2 = 0, GERBIL_ORDER_LEX = 1, GERBIL_ORDER_CGAT = 2,
+  GERBIL_ORDER_ROBERTS = 3, GERBIL_ORDER_RANDOM = 4, GERBIL_ORDER_DFP = 5
+} gerbil_ordering;
 
 typedef struct {
   uint32_t struct_size;    /* sizeof(gerbil_config); ABI versioning */
@@ -99,6 +107,8 @@ typedef struct {
                               GPU; a 1-rank communicator is created internally) */
   int32_t disable_normalization; /* 1 = `-d`: count each k-mer as it occurs;
                                     x and rc(x) are different k-mers. 0 = canonical (default) */
+  double dfp_pivot;        /* DFP ordering: pivot p in [0, 1] */
+  uint32_t order_sample_stride; /* DFP ordering: sample every stride-th 1024-base tile; 0 = 16 */
 } gerbil_config;
 
 /* Result encodings (App. C). */
@@ -224,6 +234,15 @@ gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted,
 
 /* Same, written to a file (GERBIL_E_IO if it cannot be written). */
 gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted);
+
+/* Fig. Minimizer metrics of the last count: the number of
+ * distinct k-mers (count >= min_count) per minimizer under the context's
+ * ordering — *max_per_minimizer = its maximum, *n_minimizers = minimizers
+ * owning at least one k-mer (this rank). The total number of super-mers is
+ * gerbil_stats.supermers (step (b) also cuts super-mers at 1024-window tile
+ * boundaries). Needs m <= 12; GERBIL_E_STATE before a successful count. */
+gerbil_status gerbil_minimizer_stats(gerbil_ctx* ctx, uint64_t* max_per_minimizer,
+                                     uint64_t* n_minimizers);
 
 /* Device-side view of this rank's results (valid until the next count). */
 gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers,

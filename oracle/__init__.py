@@ -37,11 +37,30 @@ def lib():
         L.oracle_supermers.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
                                        C.c_char_p, C.c_uint64]
         L.oracle_supermers.restype = C.c_uint64
+        U32P = C.POINTER(C.c_uint32)
+        L.oracle_minimizer_t.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, U32P, C.c_char_p]
+        L.oracle_order_key.argtypes = [C.c_char_p, C.c_uint32, C.c_int, U32P]
+        L.oracle_order_key.restype = C.c_uint32
+        L.oracle_supermers_t.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_int, U32P,
+                                         C.c_char_p, C.c_uint64]
+        L.oracle_supermers_t.restype = C.c_uint64
+        L.oracle_dfp_table.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, U32P]
+        L.oracle_dfp_table.restype = C.c_int
+        L.oracle_minimizer_stats.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, U32P,
+                                             C.POINTER(C.c_uint64)]
+        L.oracle_minimizer_stats.restype = C.c_int64
         _lib = L
     return _lib
 
 
-KMC2, LEX = 0, 1
+KMC2, LEX, CGAT, ROBERTS, RANDOM, DFP = 0, 1, 2, 3, 4, 5
+
+
+def _table(table):
+    """DFP key table (a dfp_table() result, or any sequence of 4^m ints) → ctypes array, or None."""
+    if table is None or isinstance(table, C.Array):
+        return table
+    return (C.c_uint32 * len(table))(*[int(x) for x in table])
 
 
 class Result:
@@ -99,18 +118,41 @@ def canonical(x: bytes) -> bytes:
     return out.raw
 
 
-def minimizer(kmer: bytes, m: int, ordering: int = KMC2, symmetric: bool = True) -> bytes:
+def minimizer(kmer: bytes, m: int, ordering: int = KMC2, symmetric: bool = True, table=None) -> bytes:
     out = C.create_string_buffer(m)
-    lib().oracle_minimizer(kmer, len(kmer), m, ordering, 1 if symmetric else 0, out)
+    lib().oracle_minimizer_t(kmer, len(kmer), m, ordering, 1 if symmetric else 0, _table(table), out)
     return out.raw
 
 
-def supermers(seq: bytes, k: int, m: int, ordering: int = LEX, symmetric: bool = False) -> list[bytes]:
+def order_key(mmer: bytes, ordering: int, table=None) -> int:
+    """The oracle's ordering key of one m-mer (x before y iff key(x) < key(y))."""
+    return lib().oracle_order_key(mmer, len(mmer), ordering, _table(table))
+
+
+def supermers(seq: bytes, k: int, m: int, ordering: int = LEX, symmetric: bool = False, table=None) -> list[bytes]:
     L = lib()
-    need = L.oracle_supermers(seq, len(seq), k, m, ordering, 1 if symmetric else 0, None, 0)
+    t = _table(table)
+    need = L.oracle_supermers_t(seq, len(seq), k, m, ordering, 1 if symmetric else 0, t, None, 0)
     buf = C.create_string_buffer(max(need, 1))
-    L.oracle_supermers(seq, len(seq), k, m, ordering, 1 if symmetric else 0, buf, need)
+    L.oracle_supermers_t(seq, len(seq), k, m, ordering, 1 if symmetric else 0, t, buf, need)
     return [s for s in buf.raw[:need].split(b"\n") if s]
+
+
+def dfp_table(text: bytes, m: int, pivot: float, stride: int):
+    """dfp(p) keys of all 4^m m-mers from the sampled frequencies (oracle_dfp_table)."""
+    out = (C.c_uint32 * (1 << (2 * m)))()
+    if lib().oracle_dfp_table(text, len(text), m, pivot, stride, out) != 0:
+        raise ValueError("parse error")
+    return out  # a ctypes uint32 array (indexable, list(out) for a copy)
+
+
+def minimizer_stats(text: bytes, k: int, m: int, ordering: int, table=None) -> tuple[int, int]:
+    """(max distinct canonical k-mers per minimizer, minimizers owning >= 1 k-mer)."""
+    n = C.c_uint64(0)
+    mx = lib().oracle_minimizer_stats(text, len(text), k, m, ordering, _table(table), C.byref(n))
+    if mx < 0:
+        raise ValueError("parse error")
+    return int(mx), n.value
 
 
 def encode_entry(kmer: bytes, count: int) -> bytes:

@@ -22,8 +22,13 @@
  *    under a total order (§2.1); super-mers = maximal substrings
  *    whose k-mers share one minimizer (Fig. 1);
  *    orderings LEX (A<C<G<T, Fig. 1) and KMC2 (A<C<G<T with the AAA/ACA
- *    prefixes demoted; reading Q9 in DESIGN.md). Pinned by the
- *    Fig. 1 example and SPEC.md:81-82 minimizer examples.
+ *    prefixes demoted; reading Q9 in DESIGN.md), and the other
+ *    orderings the paper evaluates: CGAT, Roberts, Random,
+ *    dfp(p) with its sampled frequency table (oracle_dfp_table). Pinned by the
+ *    Fig. 1 example, SPEC.md:81-82 minimizer examples, hand-ranked alphabet
+ *    examples, bijectivity and the planted-frequency dfp fixture.
+ *  - oracle_minimizer_stats: the Fig. Minimizer metric (max distinct k-mers
+ *    per minimizer), by brute force over the histogram.
  *  - oracle_count_sampled: the same histogram restricted to canonical k-mers
  *    whose FNV-1a-64 hash of the ASCII string is ≡ 0 (mod `mod`) — the
  *    full-scale parity check of SURVEY.md §8(c) "Scale strategy". Pinned by
@@ -39,6 +44,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <string>
 #include <thread>
@@ -213,10 +219,63 @@ static Result* finish(std::map<std::string, uint64_t>& hist, uint64_t windows,
 
 /* ---- minimizers and super-mers (§2.1; §3.1) ------------- */
 
+/* ---- orderings (§3.1) -------- */
+
+/* base-4 number of an m-mer string over a given letter ranking */
+static uint32_t number_in(const std::string& s, const char* alphabet) {
+  uint32_t v = 0;
+  for (char c : s) v = v * 4 + (uint32_t)(strchr(alphabet, c) - alphabet);
+  return v;
+}
+
+/* Ordering key of an m-mer (readings Q9, Q22, Q23 in DESIGN.md):
+ *  0 KMC2    A<C<G<T, m-mers starting with AAA or ACA after all others;
+ *  1 LEX     A<C<G<T (Fig. 1);
+ *  2 CGAT    lexicographic with C<G<A<T;
+ *  3 ROBERTS bases at even positions — counted from 1, i.e. the 2nd, 4th, ...
+ *            base, the reading under which "rare minimizers like CGCGCG are
+ *            preferred" holds (CGCGCG → CCCCCC) — replaced by their
+ *            complement, then lexicographic with C<A<T<G;
+ *  4 RANDOM  a fixed bijection of the A<C<G<T number v of the m-mer:
+ *            x = v*0x9E3779B1, x ^= x >> m, x = x*0x85EBCA6B, x ^= x >> m,
+ *            every product taken mod 4^m;
+ *  5 DFP     table[v] (oracle_dfp_table). */
+static uint32_t order_key_of(const std::string& mm, int ordering, const uint32_t* table) {
+  const uint32_t m = (uint32_t)mm.size();
+  const uint32_t lex = number_in(mm, "ACGT");
+  switch (ordering) {
+    case 0: {
+      const bool demoted = m >= 3 && (mm.compare(0, 3, "AAA") == 0 || mm.compare(0, 3, "ACA") == 0);
+      return lex + (demoted ? (uint32_t)(1ull << (2 * m)) : 0u);
+    }
+    case 2:
+      return number_in(mm, "CGAT");
+    case 3: {
+      std::string t = mm;
+      for (size_t i = 1; i < t.size(); i += 2) t[i] = complement(t[i]);
+      return number_in(t, "CATG");
+    }
+    case 4: {
+      const uint64_t mod = 1ull << (2 * m);
+      uint64_t x = ((uint64_t)lex * 0x9E3779B1ull) % mod;
+      x ^= x >> m;
+      x = (x * 0x85EBCA6Bull) % mod;
+      x ^= x >> m;
+      return (uint32_t)x;
+    }
+    case 5:
+      return table[lex];
+    default:
+      return lex;
+  }
+}
+
 /* Ordering "less than" on two m-mers. LEX: A<C<G<T. KMC2: the same, except
  * that m-mers starting with AAA or ACA come after all others,
- * lexicographic inside each group (reading Q9). */
-static bool order_less(const std::string& a, const std::string& b, int ordering) {
+ * lexicographic inside each group (reading Q9). Others: by order_key_of. */
+static bool order_less(const std::string& a, const std::string& b, int ordering,
+                       const uint32_t* table = nullptr) {
+  if (ordering >= 2) return order_key_of(a, ordering, table) < order_key_of(b, ordering, table);
   if (ordering == 0 && a.size() >= 3) {
     bool da = a.compare(0, 3, "AAA") == 0 || a.compare(0, 3, "ACA") == 0;
     bool db = b.compare(0, 3, "AAA") == 0 || b.compare(0, 3, "ACA") == 0;
@@ -230,16 +289,16 @@ static bool order_less(const std::string& a, const std::string& b, int ordering)
  * (PAPER.md:51). symmetric = minimum over the m-mers of x and of rc(x)
  * (reading Q7: required for canonical bins). */
 static std::string minimizer_of(const std::string& x, uint32_t m, int ordering,
-                                int symmetric) {
+                                int symmetric, const uint32_t* table = nullptr) {
   std::string best;
   bool have = false;
   std::string rx = reverse_complement(x);
   for (size_t j = 0; j + m <= x.size(); ++j) {
     std::string f = x.substr(j, m);
-    if (!have || order_less(f, best, ordering)) { best = f; have = true; }
+    if (!have || order_less(f, best, ordering, table)) { best = f; have = true; }
     if (symmetric) {
       std::string g = rx.substr(j, m);
-      if (order_less(g, best, ordering)) best = g;
+      if (order_less(g, best, ordering, table)) best = g;
     }
   }
   return best;
@@ -366,23 +425,99 @@ uint64_t oracle_encode_entry(const char* kmer, uint32_t k, uint64_t count, uint8
   return rec.size();
 }
 
-/* Minimizer m-mer of one k-mer (ordering 0 = KMC2, 1 = LEX). */
+/* Minimizer m-mer of one k-mer (ordering: see order_key_of; table = the DFP
+ * key table for ordering 5, else NULL). */
 void oracle_minimizer(const char* kmer, uint32_t k, uint32_t m, int ordering,
                       int symmetric, char* out) {
   std::string mm = minimizer_of(std::string(kmer, k), m, ordering, symmetric);
   memcpy(out, mm.data(), m);
 }
 
+void oracle_minimizer_t(const char* kmer, uint32_t k, uint32_t m, int ordering, int symmetric,
+                        const uint32_t* table, char* out) {
+  std::string mm = minimizer_of(std::string(kmer, k), m, ordering, symmetric, table);
+  memcpy(out, mm.data(), m);
+}
+
+/* Ordering key of one m-mer (order_key_of). */
+uint32_t oracle_order_key(const char* mmer, uint32_t m, int ordering, const uint32_t* table) {
+  return order_key_of(std::string(mmer, m), ordering, table);
+}
+
+/* dfp(p) key table ("we initially sort the set of minimizers by
+ * their frequency ... approximate them by taking samples during runtime ...
+ * re-sort the minimizers by the absolute difference of their initial position
+ * to the pivot position 4^m p"), reading Q23 in DESIGN.md:
+ *  sample   = every m-mer occurrence that starts in a 1024-position tile
+ *             t ≡ 0 (mod stride) of the batch (reads concatenated in input
+ *             order, every sequence character one position) and lies inside
+ *             one read with no undetermined base; each occurrence counts
+ *             for f and for rc(f);
+ *  position = rank in ascending (frequency, A<C<G<T number) order;
+ *  P        = min(4^m - 1, floor(p * 4^m));
+ *  key      = 2 (pos - P) when pos >= P, else 2 (P - pos) - 1.
+ * Writes 4^m keys (index = the A<C<G<T number); returns 0, or -1 on a parse error. */
+int oracle_dfp_table(const char* text, uint64_t len, uint32_t m, double pivot, uint32_t stride,
+                     uint32_t* out) {
+  std::vector<std::string> reads;
+  std::string e;
+  if (!parse_reads(text, len, reads, e)) return -1;
+  const uint64_t M = 1ull << (2 * m);
+  std::vector<uint64_t> freq(M, 0);
+  uint64_t base = 0;
+  for (const std::string& r : reads) {
+    std::string u = r;
+    for (char& c : u)
+      if (c >= 'a' && c <= 'z') c = (char)(c - 'a' + 'A');
+    for (size_t j = 0; j + m <= u.size(); ++j) {
+      if (((base + j) / 1024) % stride != 0) continue;
+      const std::string f = u.substr(j, m);
+      if (f.find_first_not_of("ACGT") != std::string::npos) continue;
+      freq[number_in(f, "ACGT")]++;
+      freq[number_in(reverse_complement(f), "ACGT")]++;
+    }
+    base += u.size();
+  }
+  std::vector<uint32_t> order(M);
+  for (uint64_t v = 0; v < M; ++v) order[v] = (uint32_t)v;
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return freq[a] != freq[b] ? freq[a] < freq[b] : a < b;
+  });
+  const uint64_t P = std::min<uint64_t>(M - 1, (uint64_t)std::floor(pivot * (double)M));
+  for (uint64_t pos = 0; pos < M; ++pos)
+    out[order[pos]] = (uint32_t)(pos >= P ? 2 * (pos - P) : 2 * (P - pos) - 1);
+  return 0;
+}
+
+/* Fig. Minimizer metric: number of distinct canonical
+ * k-mers per (strand-symmetric) minimizer; returns the maximum and writes the
+ * number of minimizers that own at least one k-mer. -1 on a parse error. */
+int64_t oracle_minimizer_stats(const char* text, uint64_t len, uint32_t k, uint32_t m, int ordering,
+                               const uint32_t* table, uint64_t* n_minimizers) {
+  std::vector<std::string> reads;
+  std::string e;
+  if (!parse_reads(text, len, reads, e)) return -1;
+  std::map<std::string, uint64_t> hist;
+  uint64_t windows = 0;
+  count_reads(reads, 0, reads.size(), k, 1, 1, hist, windows);
+  std::map<std::string, uint64_t> per;
+  for (auto& kv : hist) per[minimizer_of(kv.first, m, ordering, 1, table)]++;
+  uint64_t mx = 0;
+  for (auto& kv : per) mx = std::max(mx, kv.second);
+  if (n_minimizers) *n_minimizers = per.size();
+  return (int64_t)mx;
+}
+
 /* Super-mers of one ACGT-only fragment: maximal runs of consecutive k-mers
  * whose minimizers are equal (Fig. 1). Writes the super-mers
  * separated by '\n' into out (if large enough); returns the bytes needed. */
-uint64_t oracle_supermers(const char* seq, uint32_t len, uint32_t k, uint32_t m,
-                          int ordering, int symmetric, char* out, uint64_t cap) {
+uint64_t oracle_supermers_t(const char* seq, uint32_t len, uint32_t k, uint32_t m, int ordering,
+                            int symmetric, const uint32_t* table, char* out, uint64_t cap) {
   std::string s(seq, len), text;
   if (len >= k) {
     size_t nwin = len - k + 1;
     std::vector<std::string> mu(nwin);
-    for (size_t p = 0; p < nwin; ++p) mu[p] = minimizer_of(s.substr(p, k), m, ordering, symmetric);
+    for (size_t p = 0; p < nwin; ++p) mu[p] = minimizer_of(s.substr(p, k), m, ordering, symmetric, table);
     size_t p0 = 0;
     for (size_t p = 1; p <= nwin; ++p) {
       if (p == nwin || mu[p] != mu[p0]) {
@@ -395,6 +530,11 @@ uint64_t oracle_supermers(const char* seq, uint32_t len, uint32_t k, uint32_t m,
   }
   if (out && cap >= text.size()) memcpy(out, text.data(), text.size());
   return text.size();
+}
+
+uint64_t oracle_supermers(const char* seq, uint32_t len, uint32_t k, uint32_t m, int ordering,
+                          int symmetric, char* out, uint64_t cap) {
+  return oracle_supermers_t(seq, len, k, m, ordering, symmetric, nullptr, out, cap);
 }
 
 } /* extern "C" */

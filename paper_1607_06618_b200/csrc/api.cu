@@ -127,7 +127,9 @@ struct gerbil_ctx {
   DevBuf hist;  // [3][B] windows, super-mers, payload words (ull)
   DevBuf hist_all, cursor, cursor2, seg_base;
   DevBuf table, ovf, out_keys, out_counts, wave_distinct;
-  DevBuf rec_stage, rec_meta;  // streaming call: per-lane record staging; counters/snapshots/offsets
+  DevBuf rec_stage, rec_meta;
+  DevBuf order_rank, order_freq;  // DFP ordering: key table [4^m] and its sample histogram
+  uint32_t m = 0;  // streaming call: per-lane record staging; counters/snapshots/offsets
   DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
   Counters* h_counters = nullptr;  // pinned
   // results
@@ -218,6 +220,8 @@ gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_co
   if (m == 0) m = std::min<uint32_t>(7, k - 1);
   if (m > 15 || m >= k) return fail(ctx, GERBIL_E_USAGE, "m must be in [1, min(k-1, 15)]");
   if (min_count < 1) return fail(ctx, GERBIL_E_USAGE, "min_count must be >= 1");
+  if (ctx->cfg.ordering == GERBIL_ORDER_DFP && m > 12)
+    return fail(ctx, GERBIL_E_USAGE, "the DFP ordering needs m <= 12");
   return GERBIL_OK;
 }
 
@@ -534,6 +538,51 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
 }
 
 // ---------------------------------------------------------------------------
+// dfp(p) key table (reading Q23): sample m-mer
+// frequencies on the device (all ranks' samples summed), sort by (frequency,
+// A<C<G<T number), key = signed distance of the position from P = p·4^m.
+gerbil_status build_dfp_table(gerbil_ctx* ctx, const SupermerArgs& a, uint64_t n_bases, uint32_t m) {
+  const uint64_t M = 1ull << (2 * m);
+  CK(ctx->rs_bits.ensure(supermer_scratch_words(n_bases) * 8));
+  CK(ctx->order_freq.ensure(M * 4 * (ctx->comm ? ctx->world + 1 : 1)));
+  CK(ctx->order_rank.ensure(M * 4));
+  uint64_t* rs = ctx->rs_bits.as<uint64_t>();
+  uint32_t* freq = ctx->order_freq.as<uint32_t>();
+  CK(cudaMemsetAsync(freq, 0, M * 4, ctx->stream));
+  if (n_bases > 0) {
+    Timer tm(ctx, K_SUPERMER, nullptr, true, a.n_reads ? 2u : 1u);
+    CK(supermer_prepare(a, rs, ctx->stream));
+    CK(supermer_mark_reads(a, rs, 0, a.n_reads, ctx->sms, ctx->stream));
+    CK(launch_dfp_sample(a.codes, a.nmask, rs, n_bases, m, ctx->cfg.order_sample_stride, freq, ctx->sms,
+                         ctx->stream));
+  }
+  std::vector<uint64_t> f(M, 0);
+  if (ctx->comm) {  // every rank must build the same table: sum all ranks' samples
+    uint32_t* all = freq + M;
+    if (!ctx->comm->allgather(freq, all, M * 4, ctx->stream)) return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+    std::vector<uint32_t> h(M * ctx->world);
+    CK(cudaMemcpyAsync(h.data(), all, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < ctx->world; ++r)
+      for (uint64_t v = 0; v < M; ++v) f[v] += h[(size_t)r * M + v];
+  } else {
+    std::vector<uint32_t> h(M);
+    CK(cudaMemcpyAsync(h.data(), freq, M * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t v = 0; v < M; ++v) f[v] = h[v];
+  }
+  std::vector<uint32_t> order(M);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return f[x] != f[y] ? f[x] < f[y] : x < y; });
+  const uint64_t P = std::min<uint64_t>(M - 1, (uint64_t)std::floor(ctx->cfg.dfp_pivot * (double)M));
+  std::vector<uint32_t> key(M);
+  for (uint64_t pos = 0; pos < M; ++pos) key[order[pos]] = (uint32_t)(pos >= P ? 2 * (pos - P) : 2 * (P - pos) - 1);
+  CK(cudaMemcpyAsync(ctx->order_rank.p, key.data(), M * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // key is a host temporary
+  return GERBIL_OK;
+}
+
+// ---------------------------------------------------------------------------
 gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
                            const uint64_t* rstart, uint64_t n_reads, uint64_t n_bases, uint32_t k,
                            uint32_t m, uint32_t B, bool want_mu, uint64_t& n_sm) {
@@ -567,6 +616,16 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     a.bin_supermers = h + B;
     a.bin_words = ctx->comm ? h + 2 * B : nullptr;
     const UploadPlan* up = ctx->upload;
+    a.order_rank = nullptr;
+    if (ctx->cfg.ordering == GERBIL_ORDER_DFP) {
+      // dfp(p) needs the sampled frequencies before any minimizer: the whole
+      // batch must be resident (no chunk overlap for this ordering)
+      if (up)
+        for (cudaEvent_t ev : up->ev) CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
+      up = nullptr;
+      CKS(build_dfp_table(ctx, a, n_bases, m));
+      a.order_rank = ctx->order_rank.as<uint32_t>();
+    }
     if (use_reads_kernel(k, m, n_bases, n_reads)) {
       if (up)
         for (cudaEvent_t ev : up->ev) CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
@@ -631,6 +690,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   const uint32_t W = key_words(k);
   ctx->W = W;
   ctx->k = k;
+  ctx->m = m;
   uint64_t n_bases = 0;
   if (ctx->upload) {
     n_bases = ctx->upload->n_bases;  // host batch: known without waiting for the upload
@@ -871,6 +931,7 @@ void gerbil_config_default(gerbil_config* cfg) {
   cfg->struct_size = sizeof *cfg;
   cfg->device = -1;
   cfg->world = 1;
+  cfg->dfp_pivot = 0.5;
 }
 
 gerbil_status gerbil_nccl_unique_id(void* id_out, size_t id_len) {
@@ -888,6 +949,9 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
   cfg.struct_size = sizeof cfg;
   if (cfg.world < 1) cfg.world = 1;
   if (cfg.rank < 0 || cfg.rank >= cfg.world) return GERBIL_E_USAGE;
+  if (cfg.ordering < 0 || cfg.ordering > GERBIL_ORDER_DFP) return GERBIL_E_USAGE;
+  if (!(cfg.dfp_pivot >= 0.0 && cfg.dfp_pivot <= 1.0)) return GERBIL_E_USAGE;
+  if (cfg.order_sample_stride == 0) cfg.order_sample_stride = 16;
   if (cfg.world > 1 && !cfg.nccl_unique_id) return GERBIL_E_USAGE;
   if (cfg.n_bins > (1u << 20)) return GERBIL_E_USAGE;
   if (cfg.max_probes == 0) cfg.max_probes = 32;
@@ -1130,6 +1194,28 @@ gerbil_status gerbil_count(gerbil_ctx* ctx, const gerbil_reads* reads, uint32_t 
                                               pb.n_reads, k, m, min_count);
   ctx->stats.ms_reader = t_reader;
   return st;
+}
+
+gerbil_status gerbil_minimizer_stats(gerbil_ctx* ctx, uint64_t* max_per_minimizer, uint64_t* n_minimizers) {
+  if (!ctx || !max_per_minimizer || !n_minimizers) return GERBIL_E_USAGE;
+  if (!ctx->have_result) return fail(ctx, GERBIL_E_STATE, "no result: call gerbil_count first");
+  if (ctx->m > 12) return fail(ctx, GERBIL_E_USAGE, "minimizer stats need m <= 12");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t hn = 2ull << (2 * ctx->m);  // every ordering key is < 2 * 4^m
+  DevBuf hist, out;
+  CK(hist.ensure(hn * 4));
+  CK(out.ensure(16));
+  CK(cudaMemsetAsync(hist.p, 0, hn * 4, ctx->stream));
+  CK(cudaMemsetAsync(out.p, 0, 16, ctx->stream));
+  CK(launch_minimizer_hist(ctx->out_keys.as<uint64_t>(), ctx->n_out, ctx->W, ctx->k, ctx->m,
+                           (uint32_t)ctx->cfg.ordering, ctx->order_rank.as<uint32_t>(), hist.as<uint32_t>(), hn,
+                           out.as<unsigned long long>(), ctx->sms, ctx->stream));
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, out.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *max_per_minimizer = h[0];
+  *n_minimizers = h[1];
+  return GERBIL_OK;
 }
 
 gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers, const uint32_t** d_counts,

@@ -13,6 +13,7 @@ struct SupermerArgs {
   uint64_t n_reads;
   uint64_t n_bases;            // read_start[n_reads]
   uint32_t k, m, n_bins, ordering;
+  const uint32_t* order_rank;  // DFP ordering: key table [4^m] (ordering.cuh), else null
   uint32_t k_bits_for_words;   // k (payload words per super-mer = ceil((nwin+k-1)/32))
   // outputs
   uint64_t* desc;              // [cap] pos << 11 | (nwin - 1)
@@ -43,6 +44,16 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
                                cudaStream_t s);
 uint64_t supermer_tile_count(uint64_t n_bases);
 uint64_t supermer_tile_reach();
+
+// ordering.cu: dfp(p) m-mer frequency sample (freq[4^m], zeroed by the
+// caller, accumulates) and the per-minimizer distinct-k-mer histogram of a
+// result set (hist[hist_n] zeroed; out2[0] = max, out2[1] = non-empty, zeroed).
+cudaError_t launch_dfp_sample(const uint64_t* codes, const uint64_t* nmask, const uint64_t* rs_bits,
+                              uint64_t n_bases, uint32_t m, uint32_t stride, uint32_t* freq, int sms,
+                              cudaStream_t s);
+cudaError_t launch_minimizer_hist(const uint64_t* keys, uint64_t n, uint32_t W, uint32_t k, uint32_t m,
+                                  uint32_t ordering, const uint32_t* rank, uint32_t* hist, uint64_t hist_n,
+                                  unsigned long long* out2, int sms, cudaStream_t s);
 
 struct ScatterArgs {
   const uint64_t* desc_in;

@@ -35,6 +35,7 @@
 //      per persistent CTA.
 #include "common.cuh"
 #include "kernels.h"
+#include "ordering.cuh"
 
 namespace gerbil {
 namespace {
@@ -79,17 +80,6 @@ __device__ __forceinline__ uint32_t next_x(const uint32_t* n, const uint32_t* rs
   return i < limit ? i : limit;
 }
 
-// Ordering key of an m-mer value (right-aligned 2m bits). KMC2
-// (reading Q9): A<C<G<T, m-mers starting with AAA or ACA after
-// all others. LEX: plain A<C<G<T (Fig. 1).
-__device__ __forceinline__ uint32_t order_key(uint32_t v, uint32_t m, uint32_t ordering) {
-  if (ordering == 0 && m >= 3) {
-    const uint32_t pre = v >> (2 * m - 6);
-    if (pre == 0u || pre == 4u) return v | (1u << (2 * m));
-  }
-  return v;
-}
-
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -112,6 +102,7 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #ifndef GERBIL_SM_MINB
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
+template <uint32_t ORD>
 __global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,
                 int hist_smem) {
@@ -140,6 +131,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
   // sit past the N-mask's last word); words past either end stage as 0
   const int nh = a.bin_words ? 3 : 2;
   const uint32_t mmask = (uint32_t)((1ull << (2 * m)) - 1);
+  const OrderCtx ord = make_order(a.ordering, m, a.order_rank);
   const uint64_t end_p = a.n_bases >= k ? a.n_bases - k + 1 : 0;  // windows start below this
   uint32_t* h_win = s_hist;
   uint32_t* h_cnt = s_hist + B;
@@ -200,7 +192,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
           f = ((f << 2) | nb) & mmask;
           rc = (rc >> 2) | ((3u - nb) << (2 * m - 2));
         }
-        const uint32_t kf = order_key(f, m, a.ordering), kr = order_key(rc, m, a.ordering);
+        const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
         c[i] = kf < kr ? kf : kr;
       }
       uint32_t pre = 0xffffffffu;
@@ -380,15 +372,26 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
   // and spread global REDs are cheap next to this kernel's arithmetic
   const int hist_smem = a.n_bins <= 2048;
   const size_t dyn = hist_smem ? (size_t)nh * a.n_bins * sizeof(uint32_t) : 0;
-  cudaError_t e = cudaFuncSetAttribute(supermer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, supermer_kernel, kThreads, dyn);
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)sms * per_sm;
-  if (grid > t1 - t0) grid = t1 - t0;
-  supermer_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, t0, t1, hist_smem);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, dyn);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)sms * per_sm;
+    if (grid > t1 - t0) grid = t1 - t0;
+    kern<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, t0, t1, hist_smem);
+    return cudaGetLastError();
+  };
+  switch (a.ordering) {
+    case kOrdKMC2: return go(supermer_kernel<kOrdKMC2>);
+    case kOrdLEX: return go(supermer_kernel<kOrdLEX>);
+    case kOrdCGAT: return go(supermer_kernel<kOrdCGAT>);
+    case kOrdROBERTS: return go(supermer_kernel<kOrdROBERTS>);
+    case kOrdRANDOM: return go(supermer_kernel<kOrdRANDOM>);
+    case kOrdDFP: return go(supermer_kernel<kOrdDFP>);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t st) {

@@ -18,6 +18,7 @@
 // flush). Long reads (> 4096 bases on average) use the tile kernel.
 #include "common.cuh"
 #include "kernels.h"
+#include "ordering.cuh"
 
 namespace gerbil {
 namespace {
@@ -27,14 +28,6 @@ constexpr int kWarpsPerCta = 2;
 constexpr int kRing = 64;           // >= w
 constexpr int kBuf = 8;             // runs buffered per lane
 constexpr uint32_t kRunCap = 2048;  // windows per descriptor (11-bit length field)
-
-__device__ __forceinline__ uint32_t order_key_r(uint32_t v, uint32_t m, uint32_t ordering) {
-  if (ordering == 0 && m >= 3) {  // KMC2 (reading Q9)
-    const uint32_t pre = v >> (2 * m - 6);
-    if (pre == 0u || pre == 4u) return v | (1u << (2 * m));
-  }
-  return v;
-}
 
 struct WarpShared {
   uint32_t key[kRing][kLanes];
@@ -50,6 +43,7 @@ supermer_reads_kernel(SupermerArgs a, unsigned long long* work) {
   WarpShared& S = s_w[threadIdx.x >> 5];
   const uint32_t k = a.k, m = a.m, w = k - m + 1, B = a.n_bins;
   const uint32_t mmask = (uint32_t)((1ull << (2 * m)) - 1);
+  const OrderCtx ord = make_order(a.ordering, m, a.order_rank);
   const uint32_t top = 2 * m - 2;
   const uint64_t n_code_words = (a.n_bases + 31) / 32, n_mask_words = (a.n_bases + 63) / 64;
   uint64_t my_windows = 0;
@@ -143,7 +137,7 @@ supermer_reads_kernel(SupermerArgs a, unsigned long long* work) {
           f = ((f << 2) | b) & mmask;
           rc = (rc >> 2) | ((3u - b) << top);
           if (fill >= m) {
-            const uint32_t kf = order_key_r(f, m, a.ordering), kr = order_key_r(rc, m, a.ordering);
+            const uint32_t kf = order_key(f, ord), kr = order_key(rc, ord);
             c = kf < kr ? kf : kr;
           }
         }

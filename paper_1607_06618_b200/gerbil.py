@@ -21,7 +21,7 @@ _lib = C.CDLL(_LIB_PATH)
 
 OK, E_USAGE, E_IO, E_INTERNAL, E_NOMEM, E_CUDA, E_NCCL, E_STATE = range(8)
 FMT_BINARY, FMT_CSV = 0, 1
-ORDER_KMC2, ORDER_LEX = 0, 1
+ORDER_KMC2, ORDER_LEX, ORDER_CGAT, ORDER_ROBERTS, ORDER_RANDOM, ORDER_DFP = 0, 1, 2, 3, 4, 5
 
 
 class GerbilError(RuntimeError):
@@ -50,6 +50,8 @@ class Config(C.Structure):
         ("timing", C.c_int32),
         ("force_exchange", C.c_int32),
         ("disable_normalization", C.c_int32),
+        ("dfp_pivot", C.c_double),
+        ("order_sample_stride", C.c_uint32),
     ]
 
 
@@ -110,6 +112,7 @@ _lib.gerbil_nccl_unique_id.argtypes = [_P, C.c_size_t]
 _lib.gerbil_count.argtypes = [_P, C.POINTER(Reads), C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_count_device.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_count_host_packed.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
+_lib.gerbil_minimizer_stats.argtypes = [_P, _U64P, _U64P]
 _lib.gerbil_count_host_stream.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _P,
                                           C.c_uint64, _U64P]
 _lib.gerbil_pack_reads.argtypes = [C.POINTER(Reads), C.c_int32, _P, _P, _P, _U64P, _U64P, C.c_char_p, C.c_size_t]
@@ -124,14 +127,14 @@ _lib.gerbil_write_results.argtypes = [_P, C.c_char_p, C.c_int32, C.c_int]
 _lib.gerbil_debug_supermers.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32,
                                         _P, _P, _P, _P, C.c_uint64, _U64P]
 for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count_device",
-           "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
+           "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_minimizer_stats", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
            "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = [
     "gerbil_config_default", "gerbil_init", "gerbil_nccl_unique_id", "gerbil_count",
     "gerbil_count_device", "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads",
-    "gerbil_fetch",
+    "gerbil_fetch", "gerbil_minimizer_stats",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
     "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
 ]
@@ -211,7 +214,8 @@ class Gerbil:
                  world: int = 1, unique_id: bytes | None = None, comm_backend: int = 0,
                  max_probes: int = 0, distinct_ratio: float = 0.0, target_load: float = 0.0,
                  wave_table_bytes: int = 0, host_threads: int = 0, stream: int | None = None,
-                 timing: bool = False, force_exchange: bool = False, canonical: bool = True):
+                 timing: bool = False, force_exchange: bool = False, canonical: bool = True,
+                 dfp_pivot: float = 0.5, order_sample_stride: int = 0):
         cfg = Config()
         _lib.gerbil_config_default(C.byref(cfg))
         cfg.device = device
@@ -231,6 +235,8 @@ class Gerbil:
         cfg.timing = 1 if timing else 0
         cfg.force_exchange = 1 if force_exchange else 0
         cfg.disable_normalization = 0 if canonical else 1
+        cfg.dfp_pivot = dfp_pivot
+        cfg.order_sample_stride = order_sample_stride
         h = C.c_void_p()
         st = _lib.gerbil_init(C.byref(cfg), C.byref(h))
         if st != OK:
@@ -298,6 +304,12 @@ class Gerbil:
             err.needed_bytes = n.value
             raise err
         return n.value
+
+    def minimizer_stats(self) -> tuple[int, int]:
+        """(max distinct k-mers per minimizer, minimizers owning >= 1 k-mer) of the last count."""
+        mx, n = C.c_uint64(0), C.c_uint64(0)
+        self._check(_lib.gerbil_minimizer_stats(self._h, C.byref(mx), C.byref(n)))
+        return mx.value, n.value
 
     def fetch(self, sorted: bool = True, out_keys: np.ndarray | None = None,
               out_counts: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:

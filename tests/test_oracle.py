@@ -336,3 +336,75 @@ def test_output_encoding_boundaries():
     assert oracle.encode_entry(b"A" * 8, 255) == bytes([0xFF, 0, 0, 0, 255, 0, 0])
     assert oracle.encode_entry(b"T" * 9, 1) == bytes([1, 0xFF, 0xFF, 0xC0])
     assert oracle.encode_entry(b"ACGT", 2**32 - 1) == bytes([0xFF, 0xFF, 0xFF, 0xFF, 0xFF, 0x1B])
+
+
+# ---- orderings of PAPER.md:140-146 ------------------------------
+def _mmers(m):
+    return [bytes(b"ACGT"[(v >> (2 * (m - 1 - i))) & 3] for i in range(m)) for v in range(4 ** m)]
+
+
+def test_ordering_alphabets_by_hand():
+    # CGAT: C < G < A < T
+    assert [oracle.order_key(x, oracle.CGAT) for x in (b"C", b"G", b"A", b"T")] == [0, 1, 2, 3]
+    assert sorted(_mmers(2), key=lambda x: oracle.order_key(x, oracle.CGAT))[:5] == [b"CC", b"CG", b"CA", b"CT", b"GC"]
+    # Roberts: bases at even positions (the 2nd, 4th, ... — reading Q22)
+    # complemented, then C < A < T < G. Single bases are not complemented: A1 C0 G3 T2
+    assert [oracle.order_key(x, oracle.ROBERTS) for x in (b"A", b"C", b"G", b"T")] == [1, 0, 3, 2]
+    # AA → AT = (1,2) → 6; AC → AG = (1,3) → 7; CA → CT = (0,2) → 2; GT → GA = (3,1) → 13
+    assert [oracle.order_key(x, oracle.ROBERTS) for x in (b"AA", b"AC", b"CA", b"GT")] == [6, 7, 2, 13]
+    # the paper's own remark pins the reading: "rare minimizers like CGCGCG are preferred" —
+    # CGCGCG → CCCCCC is the smallest of all 6-mers
+    keys6 = {x: oracle.order_key(x, oracle.ROBERTS) for x in _mmers(6)}
+    assert min(keys6, key=keys6.get) == b"CGCGCG" and keys6[b"CGCGCG"] == 0
+
+
+def test_kmc2_and_lex_keys_agree_with_string_order():
+    # order_key (used by the tests for every ordering) agrees with the string comparison the
+    # oracle's minimizer uses for KMC2 / LEX (pinned by Fig. 1 and the SPEC examples): for every
+    # (m+1)-mer the forward minimizer is the smaller of its two m-mers under the key
+    m = 3
+    for ordering in (oracle.KMC2, oracle.LEX):
+        for z in _mmers(m + 1):
+            a, b = z[:m], z[1:]
+            want = a if oracle.order_key(a, ordering) <= oracle.order_key(b, ordering) else b
+            assert oracle.minimizer(z, m, ordering, symmetric=False) == want
+    assert [oracle.order_key(x, oracle.LEX) for x in _mmers(4)] == list(range(256))
+    # KMC2 demotes exactly the AAA / ACA prefixes
+    demoted = [x for x in _mmers(4) if oracle.order_key(x, oracle.KMC2) >= 256]
+    assert sorted(demoted) == sorted(x for x in _mmers(4) if x[:3] in (b"AAA", b"ACA"))
+
+
+def test_random_ordering_is_a_bijection():
+    for m in range(1, 8):
+        keys = [oracle.order_key(x, oracle.RANDOM) for x in _mmers(m)]
+        assert sorted(keys) == list(range(4 ** m))
+    # and it is not the identity
+    assert [oracle.order_key(x, oracle.RANDOM) for x in _mmers(3)] != list(range(64))
+
+
+def test_dfp_table_planted_frequencies():
+    # m = 1, text AAAAC: occurrences count for f and rc(f) → freq A = T = 4, C = G = 1.
+    # ascending (freq, A<C<G<T) order: C, G, A, T → positions C0 G1 A2 T3.
+    t = list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.5, 1))   # P = 2: A→0, T→2, G→1, C→3
+    assert t == [0, 3, 1, 2]
+    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.0, 1)) == [4, 0, 2, 6]  # P = 0: key = 2·pos
+    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 1.0, 1)) == [1, 5, 3, 0]  # P = 3
+    # sampling: stride 2 samples tile 0 (positions 0..1023) only
+    text = b">a\n" + b"A" * 1024 + b"C" * 1024 + b"\n"
+    t2 = list(oracle.dfp_table(text, 1, 0.0, 2))  # freq A = T = 1024, C = G = 0 → C0 G1 A2 T3
+    assert t2 == [4, 0, 2, 6]
+    t1 = list(oracle.dfp_table(text, 1, 0.0, 1))  # all: A = T = C = G = 1024 → A0 C1 G2 T3
+    assert t1 == [0, 2, 4, 6]
+    # N and read ends break m-mers: "AN" and a 1-base read give no 2-mer
+    t3 = list(oracle.dfp_table(b">a\nAN\n>b\nC\n", 2, 0.0, 1))
+    assert t3 == [2 * i for i in range(16)]  # all frequencies 0 → lexicographic positions
+
+
+def test_minimizer_stats_by_hand():
+    # all-A: one k-mer AAAA (canonical), minimizer AA
+    assert oracle.minimizer_stats(b">a\nAAAAAAAA\n", 4, 2, oracle.LEX) == (1, 1)
+    # Fig. 1 input, k = 4, m = 3, LEX, strand-symmetric: canonical 4-mers and their minimizers
+    # CAAG→AAG, AAGA→AAG, AGAA→AGA? (AGAA, rc TTCT: m-mers AGA, GAA, TTC, TCT → AGA),
+    # GAAC→AAC (rc GTTC), AACA→AAC, ACAG→ACA (rc CTGT), ACTG→ACT (rc CAGT: ACT vs AGT),
+    # AGTG→ACT (rc CACT) — 8 k-mers, minimizers {AAG:2, AGA:1, AAC:2, ACA:1, ACT:2}
+    assert oracle.minimizer_stats(b">f\nCAAGAACAGTG\n", 4, 3, oracle.LEX) == (2, 5)
