@@ -86,6 +86,14 @@ __global__ void __launch_bounds__(128) kern(uint64_t* t, uint64_t nb, int iters,
       ld256(bk, w);
       ld256(bk + 4, v);
       acc += w[0] ^ v[1] ^ w[2] ^ v[3];
+    } else if (MODE == 12 || MODE == 13) {  // key bucket load + RED into a separate counts array
+      uint64_t w[4], v[4];
+      ld256(bk, w);
+      ld256(bk + 4, v);
+      acc += w[0] ^ v[1] ^ w[2] ^ v[3];
+      unsigned* cnt = reinterpret_cast<unsigned*>(t + nb * 8);  // 16 B of counts per bucket after the keys
+      if (MODE == 12) atomicAdd(cnt + b * 4 + (acc & 3), 1u);
+      else asm volatile("red.global.add.u32 [%0], 1;" ::"l"(cnt + b * 4 + (acc & 3)) : "memory");
     } else if (MODE == 11) {  // independent pair: load of one bucket, RED into another, both random
       uint64_t w[4];
       ld256(bk, w);
@@ -104,18 +112,18 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const uint64_t nb = (uint64_t)(mib * 1048576.0 / 64);
   uint64_t *t, *sink;
-  cudaMalloc(&t, nb * 64);
+  cudaMalloc(&t, nb * 64 + nb * 16);
   cudaMalloc(&sink, 8);
-  cudaMemset(t, 0x11, nb * 64);  // non-zero: CAS(0 → x) fails, the table stays fixed
+  cudaMemset(t, 0x11, nb * 64 + nb * 16);  // non-zero: CAS(0 → x) fails, the table stays fixed
   const int grid = sms * bpsm, iters = 256;
   const double ops = (double)grid * 128 * iters;
   const char* names[] = {"load64", "load32", "red", "load+red", "cas128", "load+cas", "cg+red", "weak+red",
-                         "load+redX", "ld|red", "red+load", "ld32+redX"};
-  const double sectors[] = {2, 1, 1, 3, 1, 3, 3, 3, 3, 3, 3, 2};
+                         "load+redX", "ld|red", "red+load", "ld32+redX", "ld+redC", "ld+redC2"};
+  const double sectors[] = {2, 1, 1, 3, 1, 3, 3, 3, 3, 3, 3, 2, 3, 3};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 12; ++mode) {
+  for (int mode = 0; mode < 14; ++mode) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(a);
@@ -132,6 +140,8 @@ int main(int argc, char** argv) {
         case 9: kern<9><<<grid, 128>>>(t, nb, iters, sink); break;
         case 10: kern<10><<<grid, 128>>>(t, nb, iters, sink); break;
         case 11: kern<11><<<grid, 128>>>(t, nb, iters, sink); break;
+        case 12: kern<12><<<grid, 128>>>(t, nb, iters, sink); break;
+        case 13: kern<13><<<grid, 128>>>(t, nb, iters, sink); break;
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
