@@ -282,8 +282,24 @@ def main() -> None:
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "avg_launch_ms": avg_count_ms, "launches_per_step": st["launches_count"],
                 "share_of_step": per_kernel["count"][0] / args.steps / ms,
-                "note": "L2-resident table: the kernel is bound by L2 sector throughput/latency "
-                        "(ncu lts throughput ~55% of peak), not HBM; see DESIGN.md §4"}
+                "note": "L2-resident table: the kernel is bound by the L2 random-access rate of its "
+                        "bucket-load + atomic pattern, not HBM; see l2_ceiling and DESIGN.md §4"}
+    # The bound that applies: one 64-byte bucket load + one atomic into the same bucket per window
+    # (RED for a k-mer already present, 128-bit CAS for a new one). scripts/l2_micro.cu measured what
+    # B200's L2 sustains for exactly these patterns on a 64 MiB table (profiles/r01_l2_micro.txt).
+    L2_LOAD_RED, L2_LOAD_CAS = 49.2e9, 38.3e9  # ops/s, "load+red" / "load+cas" rows
+    new_k = float(st["distinct"])
+    hits = max(float(st["valid_windows"]) - new_k, 0.0)
+    t_floor = hits / L2_LOAD_RED + new_k / L2_LOAD_CAS
+    d_ms = per_kernel["count"][0] / args.steps  # steps (d)+(e) device time per step
+    l2_ceiling = {"bound": "l2_random_ops", "unit": "G window-ops/s",
+                  "achieved": float(st["valid_windows"]) / (d_ms / 1e3) / 1e9 if d_ms > 0 else None,
+                  "peak": float(st["valid_windows"]) / t_floor / 1e9 if t_floor > 0 else None,
+                  "frac": (t_floor * 1e3 / d_ms) if d_ms > 0 else None,
+                  "floor_ms": t_floor * 1e3, "measured_ms": d_ms,
+                  "source": "profiles/r01_l2_micro.txt (load+red 49.2, load+cas 38.3 Gop/s, 64 MiB table); "
+                            "measured_ms = steps (d)+(e) incl. compaction"}
+    roofline["l2_ceiling"] = l2_ceiling
 
     # ---- end to end through the C ABI with host buffers -----------------------------------
     e2e = None
