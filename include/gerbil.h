@@ -235,6 +235,29 @@ gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted,
 /* Same, written to a file (GERBIL_E_IO if it cannot be written). */
 gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted);
 
+/* ---- out-of-core counting ---------------------
+ * The paper's two-phase design with the temporary
+ * files in page-locked host memory, for inputs given in several batches or
+ * larger than the device: (1) gerbil_spill_begin fixes k, m and the bins
+ * (cfg.n_bins, 0 → 4096); (2) gerbil_spill_add (any number of times) runs
+ * step (b) on one HOST packed batch (layout as gerbil_count_device) and moves
+ * its super-mers, grouped by bin, to host memory owned by the context;
+ * (3) gerbil_spill_finish counts the bins in groups that fit the device
+ * budget (cfg.device_mem_cap / 2, 0 → 16 GiB per group) — every group's
+ * super-mers from every batch are uploaded, regrouped by bin and counted
+ * (steps d, e) — and streams the App. C records of every k-mer with count
+ * >= min_count into out (page-locked, as gerbil_count_host_stream; capacity 0
+ * = sizing: *n_bytes is the size needed, GERBIL_E_USAGE). The histogram is
+ * the same as one gerbil_count over the concatenated batches. No device
+ * result set remains (gerbil_fetch → GERBIL_E_STATE); stats describe the whole
+ * job. One rank only; the DFP ordering is refused (its table is per batch).
+ * GERBIL_E_STATE when called out of order. */
+gerbil_status gerbil_spill_begin(gerbil_ctx* ctx, uint32_t k, uint32_t m);
+gerbil_status gerbil_spill_add(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
+                               const uint64_t* read_start, uint64_t n_reads);
+gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* out,
+                                  uint64_t capacity, uint64_t* n_bytes);
+
 /* Fig. Minimizer metrics of the last count: the number of
  * distinct k-mers (count >= min_count) per minimizer under the context's
  * ordering — *max_per_minimizer = its maximum, *n_minimizers = minimizers

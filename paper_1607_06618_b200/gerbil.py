@@ -113,6 +113,9 @@ _lib.gerbil_count.argtypes = [_P, C.POINTER(Reads), C.c_uint32, C.c_uint32, C.c_
 _lib.gerbil_count_device.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_count_host_packed.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_minimizer_stats.argtypes = [_P, _U64P, _U64P]
+_lib.gerbil_spill_begin.argtypes = [_P, C.c_uint32, C.c_uint32]
+_lib.gerbil_spill_add.argtypes = [_P, _P, _P, _P, C.c_uint64]
+_lib.gerbil_spill_finish.argtypes = [_P, C.c_uint32, _P, C.c_uint64, _U64P]
 _lib.gerbil_count_host_stream.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _P,
                                           C.c_uint64, _U64P]
 _lib.gerbil_pack_reads.argtypes = [C.POINTER(Reads), C.c_int32, _P, _P, _P, _U64P, _U64P, C.c_char_p, C.c_size_t]
@@ -127,14 +130,15 @@ _lib.gerbil_write_results.argtypes = [_P, C.c_char_p, C.c_int32, C.c_int]
 _lib.gerbil_debug_supermers.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32,
                                         _P, _P, _P, _P, C.c_uint64, _U64P]
 for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count_device",
-           "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_minimizer_stats", "gerbil_pack_reads", "gerbil_fetch", "gerbil_results_device",
+           "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_minimizer_stats", "gerbil_pack_reads",
+           "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish", "gerbil_fetch", "gerbil_results_device",
            "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = [
     "gerbil_config_default", "gerbil_init", "gerbil_nccl_unique_id", "gerbil_count",
     "gerbil_count_device", "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads",
-    "gerbil_fetch", "gerbil_minimizer_stats",
+    "gerbil_fetch", "gerbil_minimizer_stats", "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
     "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
 ]
@@ -299,6 +303,26 @@ class Gerbil:
         rc = _lib.gerbil_count_host_stream(self._h, _ptr(codes), _ptr(nmask), _ptr(read_start), n_reads, k, m,
                                            min_count, _ptr(out) if out is not None else None, cap, C.byref(n))
         self.k = k
+        if rc != 0:
+            err = GerbilError(rc, _lib.gerbil_last_error(self._h).decode(errors="replace"))
+            err.needed_bytes = n.value
+            raise err
+        return n.value
+
+    # ---- out-of-core counting (include/gerbil.h gerbil_spill_*) ---------------
+    def spill_begin(self, k: int, m: int = 0) -> None:
+        self._check(_lib.gerbil_spill_begin(self._h, k, m))
+        self.k = k
+
+    def spill_add(self, codes, nmask, read_start, n_reads: int) -> None:
+        self._check(_lib.gerbil_spill_add(self._h, _ptr(codes), _ptr(nmask), _ptr(read_start), n_reads))
+
+    def spill_finish(self, min_count: int = 1, out: np.ndarray | None = None) -> int:
+        """Phase two; App. C records into `out` (page-locked uint8 array). Returns the record bytes;
+        GerbilError with needed_bytes when `out` is missing or too small."""
+        n = C.c_uint64(0)
+        cap = 0 if out is None else out.nbytes
+        rc = _lib.gerbil_spill_finish(self._h, min_count, _ptr(out) if out is not None else None, cap, C.byref(n))
         if rc != 0:
             err = GerbilError(rc, _lib.gerbil_last_error(self._h).decode(errors="replace"))
             err.needed_bytes = n.value
