@@ -108,17 +108,60 @@ struct SpillBatch {
   uint64_t n_sm = 0, n_words = 0;
   std::vector<uint64_t> d_off, w_off;  // [B+1] per-bin offsets into desc / payload
 };
+// Page-locked blocks reused across spill jobs: pinning host memory costs far
+// more than the PCIe copies themselves (~2 GB/s), so blocks go back to the
+// pool instead of being freed.
+struct PinnedPool {
+  std::vector<std::pair<void*, size_t>> free_blocks;
+  void* get(size_t n) {
+    size_t best = SIZE_MAX, bi = 0;
+    for (size_t i = 0; i < free_blocks.size(); ++i)
+      if (free_blocks[i].second >= n && free_blocks[i].second < best) best = free_blocks[i].second, bi = i;
+    if (best != SIZE_MAX) {
+      void* p = free_blocks[bi].first;
+      free_blocks.erase(free_blocks.begin() + bi);
+      sizes.push_back({p, best});
+      return p;
+    }
+    void* p = nullptr;
+    const size_t want = n + n / 8 + 4096;  // room for a slightly larger batch next time
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    sizes.push_back({p, want});
+    return p;
+  }
+  void put(void* p) {
+    if (!p) return;
+    for (size_t i = 0; i < sizes.size(); ++i)
+      if (sizes[i].first == p) {
+        free_blocks.push_back(sizes[i]);
+        sizes.erase(sizes.begin() + i);
+        return;
+      }
+  }
+  void clear() {
+    for (auto& b : free_blocks) cudaFreeHost(b.first);
+    for (auto& b : sizes) cudaFreeHost(b.first);
+    free_blocks.clear();
+    sizes.clear();
+  }
+  std::vector<std::pair<void*, size_t>> sizes;  // blocks in use
+};
+
 struct SpillState {
   bool active = false;
   uint32_t k = 0, m = 0, B = 0;
   std::vector<SpillBatch> batches;
   std::vector<uint64_t> win, cnt, words;  // [B] totals over batches
   uint64_t bases = 0, reads = 0, windows = 0, supermers = 0;
-  void release() {
+  PinnedPool pool;
+  void release() {  // blocks return to the pool
     for (auto& b : batches) {
-      if (b.desc) cudaFreeHost(b.desc);
-      if (b.bin) cudaFreeHost(b.bin);
-      if (b.payload) cudaFreeHost(b.payload);
+      pool.put(b.desc);
+      pool.put(b.bin);
+      pool.put(b.payload);
     }
     batches.clear();
     active = false;
@@ -1044,6 +1087,7 @@ void gerbil_finalize(gerbil_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   delete ctx->comm;
   ctx->spill.release();
+  ctx->spill.pool.clear();
   if (ctx->lane_stream) {
     cudaStreamSynchronize(ctx->lane_stream);
     cudaStreamDestroy(ctx->lane_stream);
@@ -1205,7 +1249,10 @@ gerbil_status gerbil_spill_begin(gerbil_ctx* ctx, uint32_t k, uint32_t m) {
     return fail(ctx, GERBIL_E_USAGE, "out-of-core counting needs a data-independent ordering (not DFP)");
   ctx->spill.release();
   SpillState& sp = ctx->spill;
-  sp = SpillState();
+  sp.win.clear();
+  sp.cnt.clear();
+  sp.words.clear();
+  sp.bases = sp.reads = sp.windows = sp.supermers = 0;
   sp.active = true;
   sp.k = k;
   sp.m = m;
@@ -1288,9 +1335,15 @@ gerbil_status gerbil_spill_add(gerbil_ctx* ctx, const uint64_t* codes, const uin
   }
   // spill to page-locked host memory (the temporary files)
   if (n_sm) {
-    CK(cudaHostAlloc((void**)&sb.desc, n_sm * 8, cudaHostAllocDefault));
-    CK(cudaHostAlloc((void**)&sb.bin, n_sm * 4, cudaHostAllocDefault));
-    CK(cudaHostAlloc((void**)&sb.payload, std::max<uint64_t>(sb.n_words, 1) * 8, cudaHostAllocDefault));
+    sb.desc = static_cast<uint64_t*>(sp.pool.get(n_sm * 8));
+    sb.bin = static_cast<uint32_t*>(sp.pool.get(n_sm * 4));
+    sb.payload = static_cast<uint64_t*>(sp.pool.get(std::max<uint64_t>(sb.n_words, 1) * 8));
+    if (!sb.desc || !sb.bin || !sb.payload) {
+      sp.pool.put(sb.desc);
+      sp.pool.put(sb.bin);
+      sp.pool.put(sb.payload);
+      return fail(ctx, GERBIL_E_NOMEM, "spill: cannot page-lock host memory");
+    }
     CK(cudaMemcpyAsync(sb.desc, ctx->send_desc.p, n_sm * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(sb.bin, ctx->send_bin.p, n_sm * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(sb.payload, ctx->send_payload.p, sb.n_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1326,6 +1379,7 @@ gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* 
   }
   CK(cudaSetDevice(ctx->device));
   const uint32_t k = sp.k, B = sp.B;
+  trace("call");
   begin_call(ctx);
   memset(&ctx->stats, 0, sizeof ctx->stats);
   ctx->W = key_words(k);
@@ -1401,8 +1455,10 @@ gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* 
       gd += d1 - d0;
       gw += w1 - w0;
     }
+    trace("spill group uploaded + regrouped (issued)");
     st = count_waves(ctx, ctx->recv_payload.as<uint64_t>(), ctx->desc_sorted.as<uint64_t>(), bin_off, bin_win,
                      owned, k, min_count, g_windows);
+    trace("spill group counted");
     if (st != GERBIL_OK) break;
     if (ctx->stats.count_sum != g_windows) {
       st = fail(ctx, GERBIL_E_INTERNAL, "invariant violated in a spill group: sum of counts != windows");
