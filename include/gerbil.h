@@ -235,6 +235,25 @@ gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted,
 /* Same, written to a file (GERBIL_E_IO if it cannot be written). */
 gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted);
 
+/* ---- step (a) on the device --------------------
+ * "Phase one on the GPU" (the paper's future work): a FASTA /
+ * FASTQ / raw document (App. B) is parsed by kernels into the
+ * packed batch layout above — identical, bit for bit, to gerbil_pack_reads
+ * on the same text (readings Q3/Q4). text is host memory (on_device = 0,
+ * copied to the device; page-locked for full PCIe speed) or device memory
+ * (on_device = 1, not modified). gerbil_parse_text returns the batch in host
+ * arrays sized as for gerbil_pack_reads (NULL arrays: only *n_bases and
+ * *n_reads — the sizing call). gerbil_count_text runs steps (a)…(e) on the
+ * device (results as after gerbil_count_device). GERBIL_E_IO (message with
+ * the line number) for malformed FASTQ, and for FASTQ with empty lines
+ * between records, which the device parser does not take (the host reader
+ * does). */
+gerbil_status gerbil_parse_text(gerbil_ctx* ctx, const char* text, uint64_t len, int32_t on_device,
+                                uint64_t* codes, uint64_t* nmask, uint64_t* read_start,
+                                uint64_t* n_bases, uint64_t* n_reads);
+gerbil_status gerbil_count_text(gerbil_ctx* ctx, const char* text, uint64_t len, int32_t on_device,
+                                uint32_t k, uint32_t m, uint32_t min_count);
+
 /* ---- out-of-core counting ---------------------
  * The paper's two-phase design with the temporary
  * files in page-locked host memory, for inputs given in several batches or

@@ -48,6 +48,29 @@ uint64_t supermer_tile_reach();
 // ordering.cu: dfp(p) m-mer frequency sample (freq[4^m], zeroed by the
 // caller, accumulates) and the per-minimizer distinct-k-mer histogram of a
 // result set (hist[hist_n] zeroed; out2[0] = max, out2[1] = non-empty, zeroed).
+// parse.cu: step (a) on the device (FASTA/FASTQ/raw text → packed batch); api.cu
+// gerbil_parse_text orchestrates. Error codes of classify (low 8 bits of *err,
+// line index above): 1 expected '@', 2 expected '+', 3 quality length,
+// 4 truncated record, 5 empty line between FASTQ records.
+uint64_t parse_blocks(uint64_t len);
+uint64_t scan_tmp_words(uint64_t n);
+cudaError_t launch_parse_count(const uint8_t* t, uint64_t len, uint32_t* cnt_nl, uint32_t* cnt_cr, cudaStream_t s);
+cudaError_t launch_widen(const uint32_t* a, uint64_t* b, uint64_t n, int sms, cudaStream_t s);
+cudaError_t launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* tmp, uint64_t* total,
+                            cudaStream_t s);
+cudaError_t launch_parse_write(const uint8_t* t, uint64_t len, const uint64_t* off_nl, const uint64_t* off_cr,
+                               uint64_t* line_start, uint64_t* cr_pos, cudaStream_t s);
+cudaError_t launch_parse_lines(const uint8_t* t, const uint64_t* ls, uint64_t n_lines, const uint64_t* cr,
+                               uint64_t n_cr, uint32_t* eff, uint8_t* first,
+                               unsigned long long* first_nonempty /* [2]: min, max */, int sms, cudaStream_t s);
+cudaError_t launch_parse_classify(const uint32_t* eff, const uint8_t* first, uint64_t n_lines, uint64_t f0,
+                                  uint64_t n_eff, int kind, uint64_t* seq_len, uint64_t* rflag,
+                                  unsigned long long* err, int sms, cudaStream_t s);
+cudaError_t launch_parse_read_starts(const uint64_t* pos, const uint64_t* rflag, const uint64_t* ridx,
+                                     uint64_t n_lines, uint64_t* read_start, int sms, cudaStream_t s);
+cudaError_t launch_parse_pack(const uint8_t* t, const uint64_t* ls, const uint64_t* seq_len, const uint64_t* pos,
+                              uint64_t n_lines, uint64_t* codes, uint64_t* nmask, int sms, cudaStream_t s);
+
 cudaError_t launch_dfp_sample(const uint64_t* codes, const uint64_t* nmask, const uint64_t* rs_bits,
                               uint64_t n_bases, uint32_t m, uint32_t stride, uint32_t* freq, int sms,
                               cudaStream_t s);

@@ -114,6 +114,8 @@ _lib.gerbil_count_device.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c
 _lib.gerbil_count_host_packed.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_minimizer_stats.argtypes = [_P, _U64P, _U64P]
 _lib.gerbil_spill_begin.argtypes = [_P, C.c_uint32, C.c_uint32]
+_lib.gerbil_parse_text.argtypes = [_P, _P, C.c_uint64, C.c_int32, _P, _P, _P, _U64P, _U64P]
+_lib.gerbil_count_text.argtypes = [_P, _P, C.c_uint64, C.c_int32, C.c_uint32, C.c_uint32, C.c_uint32]
 _lib.gerbil_spill_add.argtypes = [_P, _P, _P, _P, C.c_uint64]
 _lib.gerbil_spill_finish.argtypes = [_P, C.c_uint32, _P, C.c_uint64, _U64P]
 _lib.gerbil_count_host_stream.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _P,
@@ -131,7 +133,8 @@ _lib.gerbil_debug_supermers.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32, 
                                         _P, _P, _P, _P, C.c_uint64, _U64P]
 for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count_device",
            "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_minimizer_stats", "gerbil_pack_reads",
-           "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish", "gerbil_fetch", "gerbil_results_device",
+           "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish", "gerbil_parse_text",
+           "gerbil_count_text", "gerbil_fetch", "gerbil_results_device",
            "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
     getattr(_lib, _f).restype = C.c_int
 
@@ -139,6 +142,7 @@ EXPORTED = [
     "gerbil_config_default", "gerbil_init", "gerbil_nccl_unique_id", "gerbil_count",
     "gerbil_count_device", "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_pack_reads",
     "gerbil_fetch", "gerbil_minimizer_stats", "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish",
+    "gerbil_parse_text", "gerbil_count_text",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
     "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
 ]
@@ -308,6 +312,39 @@ class Gerbil:
             err.needed_bytes = n.value
             raise err
         return n.value
+
+    # ---- step (a) on the device (include/gerbil.h gerbil_parse_text / gerbil_count_text) ----
+    @staticmethod
+    def _text_arg(text):
+        """bytes / numpy uint8 (host) or a CUDA uint8 tensor → (pointer, length, on_device, keepalive)."""
+        if isinstance(text, (bytes, bytearray)):
+            buf = C.create_string_buffer(bytes(text), len(text))
+            return C.cast(buf, C.c_void_p).value, len(text), 0, buf
+        if isinstance(text, np.ndarray):
+            return text.ctypes.data, text.nbytes, 0, text
+        # torch tensor
+        on_dev = 1 if getattr(text, "is_cuda", False) else 0
+        return text.data_ptr(), text.numel() * text.element_size(), on_dev, text
+
+    def parse_text(self, text) -> PackedReads:
+        """Parse FASTA / FASTQ / raw text on the GPU → the packed batch (host arrays)."""
+        ptr, n, dev, keep = self._text_arg(text)
+        nb, nr = C.c_uint64(), C.c_uint64()
+        self._check(_lib.gerbil_parse_text(self._h, ptr, n, dev, None, None, None, C.byref(nb), C.byref(nr)))
+        codes = np.zeros(max((nb.value + 31) // 32, 1), np.uint64)
+        nmask = np.zeros(max((nb.value + 63) // 64, 1), np.uint64)
+        rs = np.zeros(nr.value + 1, np.uint64)
+        self._check(_lib.gerbil_parse_text(self._h, ptr, n, dev, _ptr(codes), _ptr(nmask), _ptr(rs), C.byref(nb),
+                                           C.byref(nr)))
+        del keep
+        return PackedReads(codes, nmask, rs, nb.value, nr.value)
+
+    def count_text(self, text, k: int, m: int = 0, min_count: int = 1) -> None:
+        """Steps (a)..(e) on the GPU from FASTA / FASTQ / raw text (host bytes or a CUDA uint8 tensor)."""
+        ptr, n, dev, keep = self._text_arg(text)
+        self._check(_lib.gerbil_count_text(self._h, ptr, n, dev, k, m, min_count))
+        self.k = k
+        del keep
 
     # ---- out-of-core counting (include/gerbil.h gerbil_spill_*) ---------------
     def spill_begin(self, k: int, m: int = 0) -> None:
