@@ -33,7 +33,17 @@ UNIT = "bases/s"
 # configs[1]: "F. vesca-scale synthetic Illumina reads (~5 Gbp, 100-bp), k=40, 1xB200"
 C1 = dict(seed=2, genome_len=240_000_000, read_len=100, n_reads=50_000_000, err=0.0033, nrate=0.0001)
 K, M, MIN_COUNT = 40, 7, 1
-WORKLOAD_NAME = "C1: F. vesca-scale synthetic Illumina reads, 5e7 x 100 bp = 5 Gbp per GPU, k=40, m=7, min_count=1"
+WORKLOAD_NAME = ""
+
+
+def set_m(m: int) -> None:
+    global M, WORKLOAD_NAME
+    M = m
+    WORKLOAD_NAME = (f"C1: F. vesca-scale synthetic Illumina reads, 5e7 x 100 bp = 5 Gbp per GPU, k=40, m={m}, "
+                     "min_count=1")
+
+
+set_m(M)
 ORACLE_SAMPLE_READS = 100_000  # 10 Mbp per oracle step: ~10 s of single-thread std::map work
 
 
@@ -174,7 +184,10 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--table-mb", type=int, default=0)
     ap.add_argument("--bins", type=int, default=0)
+    ap.add_argument("--m", type=int, default=M, help="minimizer length (results are invariant in m)")
+    ap.add_argument("--count-mode", type=int, default=0, help="gerbil_config.count_mode (0 auto, 1 L2, 2 smem)")
     args = ap.parse_args()
+    set_m(args.m)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -200,10 +213,10 @@ def main() -> None:
         obj = [gerbil.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    n_bins = args.bins or (4096 if world > 1 else 0)
+    n_bins = args.bins or ((1 << 20 if M >= 11 else 4096) if world > 1 else 0)
     g = gerbil.Gerbil(device=local, rank=rank, world=world, unique_id=uid, n_bins=n_bins,
                       stream=stream.cuda_stream, timing=True,
-                      wave_table_bytes=args.table_mb << 20)
+                      wave_table_bytes=args.table_mb << 20, count_mode=args.count_mode)
 
     w = synth.Workload(**{**C1, "n_reads": args.reads, "first_read": rank * args.reads})
     codes, nmask, rs = synth.packed_device(w, device=dev, stream=stream.cuda_stream)
@@ -360,7 +373,9 @@ def main() -> None:
                        "valid_windows": st["valid_windows"], "ratio_observed": st["ratio_observed"],
                        "overflow_kmers": st["overflow_kmers"],
                        "first_probe_frac": st["probe_first"] / max(st["probe_first"] + st["probe_more"], 1),
-                       "max_probes": st["probe_max"]},
+                       "max_probes": st["probe_max"], "smem_bins": st["smem_bins"],
+                       "smem_failed": st["smem_failed"], "smem_windows": st["smem_windows"],
+                       "smem_slots": st["smem_slots"]},
             "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clocks,

@@ -109,6 +109,15 @@ typedef struct {
                                     x and rc(x) are different k-mers. 0 = canonical (default) */
   double dfp_pivot;        /* DFP ordering: pivot p in [0, 1] */
   uint32_t order_sample_stride; /* DFP ordering: sample every stride-th 1024-base tile; 0 = 16 */
+  int32_t count_mode;      /* step (d) table placement:
+                              0 = auto: a bin predicted (ρ̂ · windows) to fit one warp's
+                                  shared-memory table is counted there, the rest in
+                                  L2-resident wave tables; n_bins = 0 then picks enough bins
+                                  (up to 2^20) when m >= 11 makes bins that small;
+                              1 = L2 wave tables only;
+                              2 = try shared memory for every bin (test seam: bins that
+                                  overflow it are recounted in the wave tables).
+                              Results never depend on it. Streaming calls use 1. */
 } gerbil_config;
 
 /* Result encodings (App. C). */
@@ -154,6 +163,11 @@ typedef struct {
   /* host reader (step a) wall milliseconds */
   double ms_reader;
   uint32_t launches_count, launches_compact, launches_total;
+  /* step (d) in shared memory (count_mode != 1) */
+  uint64_t smem_bins;        /* bins counted in per-warp shared-memory tables */
+  uint64_t smem_failed;      /* of which abandoned (too many distinct k-mers) and recounted in L2 */
+  uint64_t smem_windows;     /* windows of the bins that completed in shared memory */
+  uint32_t smem_slots;       /* table slots per warp */
 } gerbil_stats;
 
 /* Fills cfg with defaults (struct_size set, everything else "auto"). */

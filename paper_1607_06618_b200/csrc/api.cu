@@ -202,6 +202,8 @@ struct gerbil_ctx {
   DevBuf text_buf, p_cnt, p_off, p_ls, p_cr, p_eff, p_first, p_seq, p_rflag, p_pos, p_ridx, p_tmp, p_misc;  // parser
   uint32_t m = 0;  // streaming call: per-lane record staging; counters/snapshots/offsets
   DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
+  DevBuf smem_range, smem_failed, rest_desc, rest_range, rest_off;  // step (d) in shared memory
+  int smem_optin = 0;  // max dynamic shared memory per block (bytes)
   Counters* h_counters = nullptr;  // pinned
   // results
   bool have_result = false;
@@ -299,8 +301,22 @@ gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_co
   return GERBIL_OK;
 }
 
-uint32_t choose_bins(const gerbil_ctx* ctx, uint64_t n_bases, uint32_t W) {
+uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k);
+
+uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, uint32_t m) {
   if (ctx->cfg.n_bins) return ctx->cfg.n_bins;
+  // Shared-memory counting (count_smem.cu) wants bins whose distinct k-mers
+  // fit one warp's table: ~0.35 of its slots on average leaves room for
+  // skew. Bins are hashes of minimizers, so that needs many more minimizers
+  // than bins (m >= 11: >= 2M canonical m-mers) — else the L2 policy below.
+  const uint32_t cap = (ctx->rec_out || m < 11) ? 0u : smem_slots_for(ctx, k);
+  if (cap) {
+    const double want = ctx->rho * (double)n_bases * ctx->world / (0.35 * cap);
+    uint32_t B = 512;
+    while ((double)B < want && B < (1u << 20)) B <<= 1;
+    while (B < 64u * (uint32_t)ctx->world) B <<= 1;
+    return B;
+  }
   // Enough bins that one L2-sized wave packs ~16 of them (waves are unions of
   // whole bins), at least 512 (the paper's default F) and at
   // least 64 per rank.
@@ -330,11 +346,32 @@ void trace(const char* what) {
 }
 
 // ---------------------------------------------------------------------------
-// Steps (d)+(e) over the bin-ordered descriptors of this rank.
-gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
-                          const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
-                          const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
-                          uint64_t total_windows) {
+// Grow b to n bytes keeping its first `keep` bytes (results of an earlier pass).
+cudaError_t ensure_keep(DevBuf& b, size_t n, size_t keep, cudaStream_t s) {
+  if (n <= b.bytes && b.p) return cudaSuccess;
+  if (keep == 0 || !b.p) return b.ensure(n);
+  DevBuf nb;
+  cudaError_t e = nb.ensure(n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  std::swap(b.p, nb.p);
+  std::swap(b.bytes, nb.bytes);
+  return cudaSuccess;
+}
+
+// Results already produced by the shared-memory pass of this call: the wave
+// pass appends after them (out_n, Σcount and distinct start from these).
+struct Preset {
+  unsigned long long out_n = 0, sum_counts = 0, distinct = 0;
+};
+
+// Steps (d)+(e) in L2-resident wave tables over the bin-ordered descriptors
+// of `bins` (consecutive in desc).
+gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
+                             const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
+                             const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
+                             uint64_t total_windows, const Preset& pre) {
   const uint32_t W = key_words(k);
   const uint64_t bb = table_inline(k) ? kInlineBucketBytes : table_bucket_bytes(k);
   const double slot_bytes = (double)bb / kSlotsPerBucket;
@@ -379,9 +416,9 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     const uint64_t lane_bytes = (max_nb * bb + 255) & ~255ull;
     CK(ctx->table.ensure(lanes * lane_bytes));
     CK(ctx->ovf.ensure(ovf_cap * W * 8));
-    const uint64_t out_cap = out_bound + ovf_cap;
-    CK(ctx->out_keys.ensure(out_cap * W * 8));
-    CK(ctx->out_counts.ensure(out_cap * 4));
+    const uint64_t out_cap = pre.out_n + out_bound + ovf_cap;
+    CK(ensure_keep(ctx->out_keys, out_cap * W * 8, pre.out_n * W * 8, ctx->stream));
+    CK(ensure_keep(ctx->out_counts, out_cap * 4, pre.out_n * 4, ctx->stream));
     // [0, n): distinct per wave; [n, 2n): dynamic work counters of the count launches
     const size_t nw = std::max<size_t>(waves.size(), 1);
     CK(ctx->wave_distinct.ensure(2 * nw * 8));
@@ -389,6 +426,16 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, 2 * nw * 8, ctx->stream));
     Counters* dc = ctx->counters.as<Counters>();
     CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
+    if (pre.out_n || pre.sum_counts || pre.distinct) {
+      static_assert(offsetof(Counters, sum_counts) == offsetof(Counters, out_n) + 8 &&
+                        offsetof(Counters, distinct) == offsetof(Counters, out_n) + 16,
+                    "preset copy assumes out_n, sum_counts, distinct are adjacent");
+      hc.out_n = pre.out_n;  // pinned staging for the copy
+      hc.sum_counts = pre.sum_counts;
+      hc.distinct = pre.distinct;
+      CK(cudaMemcpyAsync(&dc->out_n, &hc.out_n, 24, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
 
     TableArgs t{};
     t.table = ctx->table.as<unsigned char>();
@@ -612,6 +659,160 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   }
 }
 
+// Shared-memory table slots per warp for this k (0 = shared-memory path off).
+uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
+  if (ctx->cfg.count_mode == 1) return 0;
+  if (!ctx->smem_optin &&
+      cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const uint32_t cap = smem_table_slots(k, (size_t)ctx->smem_optin - 1024);
+  return cap >= 128 ? cap : 0;
+}
+
+// Steps (d)+(e) over the bin-ordered descriptors of this rank. Bins predicted
+// (ρ̂ · windows) to fit one warp's shared-memory table are counted there, in
+// one launch (count_smem.cu); the others — and any bin the shared-memory pass
+// abandoned — are gathered into one contiguous descriptor range and counted in
+// the L2-resident wave tables, whose results are appended.
+gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
+                          const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
+                          const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
+                          uint64_t total_windows) {
+  const uint32_t W = key_words(k);
+  const uint32_t cap = ctx->rec_out ? 0u : smem_slots_for(ctx, k);
+  ctx->stats.smem_slots = cap;
+  if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
+                                      total_windows, Preset{});
+  const uint32_t max_fill = cap - std::max<uint32_t>(32u, cap / 4);
+  const bool force = ctx->cfg.count_mode == 2;
+  std::vector<uint32_t> elig, rest;
+  for (uint32_t b : bins) {
+    if (bin_off[b + 1] == bin_off[b]) continue;  // no super-mers, nothing to count
+    // predicted distinct (ρ̂ · windows) within the abandonment threshold; a miss costs
+    // only the bin's partial work (it is recounted in the wave tables)
+    const bool fits = bin_win[b] <= max_fill || ctx->rho * (double)bin_win[b] <= 0.95 * max_fill;
+    (force || fits ? elig : rest).push_back(b);
+  }
+  if (elig.empty())
+    return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count, total_windows,
+                          Preset{});
+  // heaviest first: the static round-robin gives every warp a similar mix
+  std::stable_sort(elig.begin(), elig.end(), [&](uint32_t a, uint32_t b) { return bin_win[a] > bin_win[b]; });
+  const uint32_t n = (uint32_t)elig.size();
+  std::vector<unsigned long long> rng(2 * (size_t)n);
+  uint64_t out_bound = 0, elig_windows = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t b = elig[i];
+    rng[2 * i] = bin_off[b];
+    rng[2 * i + 1] = bin_off[b + 1] | (std::min<uint64_t>(bin_win[b], (1u << 24) - 1) << kRangeWinShift);
+    out_bound += std::min<uint64_t>(bin_win[b], max_fill);
+    elig_windows += bin_win[b];
+  }
+  CK(ctx->smem_range.ensure(rng.size() * 8));
+  CK(ctx->smem_failed.ensure((size_t)n * 4 + 8));
+  CK(ctx->out_keys.ensure(std::max<uint64_t>(out_bound, 1) * W * 8));
+  CK(ctx->out_counts.ensure(std::max<uint64_t>(out_bound, 1) * 4));
+  CK(ctx->counters.ensure(sizeof(Counters)));
+  CK(cudaMemcpyAsync(ctx->smem_range.p, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  Counters* dc = ctx->counters.as<Counters>();
+  CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
+  CK(cudaMemsetAsync(&dc->read_work, 0, 8, ctx->stream));  // n_failed
+  SmemCountArgs a{};
+  a.codes = stream_codes;
+  a.desc = desc;
+  a.range = ctx->smem_range.as<unsigned long long>();
+  a.n_list = n;
+  a.k = k;
+  a.min_count = min_count;
+  a.canonical = ctx->cfg.disable_normalization ? 0u : 1u;
+  a.cap = cap;
+  a.max_fill = max_fill;
+  a.out_keys = ctx->out_keys.as<uint64_t>();
+  a.out_counts = ctx->out_counts.as<uint32_t>();
+  a.out_cap = out_bound;
+  a.out_n = &dc->out_n;
+  a.sum_counts = &dc->sum_counts;
+  a.distinct = &dc->distinct;
+  a.failed = ctx->smem_failed.as<uint32_t>();
+  a.n_failed = &dc->read_work;
+  {
+    Timer tm(ctx, K_COUNT);
+    CK(launch_count_smem(a, ctx->sms, ctx->stream));
+  }
+  Counters& hc = *ctx->h_counters;
+  CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hc.out_n > out_bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+  const uint64_t n_failed = hc.read_work;
+  Preset pre;
+  pre.out_n = hc.out_n;
+  pre.sum_counts = hc.sum_counts;
+  pre.distinct = hc.distinct;
+  std::vector<uint32_t> failed(n_failed);
+  if (n_failed) {
+    CK(cudaMemcpyAsync(failed.data(), ctx->smem_failed.p, n_failed * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  uint64_t failed_windows = 0;
+  for (uint32_t li : failed) {
+    rest.push_back(elig[li]);
+    failed_windows += bin_win[elig[li]];
+  }
+  ctx->stats.smem_bins += n;
+  ctx->stats.smem_failed += n_failed;
+  const uint64_t smem_windows = elig_windows - failed_windows;
+  ctx->stats.smem_windows += smem_windows;
+  const double smem_obs = smem_windows ? (double)pre.distinct / (double)smem_windows : 0.0;
+  gerbil_status st = GERBIL_OK;
+  if (rest.empty()) {
+    ctx->stats.waves = 0;
+    ctx->stats.ratio_used = ctx->rho;
+    ctx->stats.ratio_observed = smem_obs;
+    ctx->stats.overflow_kmers = 0;
+    ctx->stats.overflow_passes = 0;
+    ctx->n_out = pre.out_n;
+    ctx->stats.kept = pre.out_n;
+    ctx->stats.distinct = pre.distinct;
+    ctx->stats.count_sum = pre.sum_counts;
+    ctx->stats.owned_windows = total_windows;
+  } else {
+    // gather the remaining bins' descriptors into one contiguous range
+    std::sort(rest.begin(), rest.end());
+    const uint32_t R = (uint32_t)rest.size();
+    std::vector<unsigned long long> rr(2 * (size_t)R), ro(R);
+    std::vector<uint64_t> off2(R + 1, 0), win2(R);
+    std::vector<uint32_t> list2(R);
+    for (uint32_t i = 0; i < R; ++i) {
+      const uint32_t b = rest[i];
+      rr[2 * i] = bin_off[b];
+      rr[2 * i + 1] = bin_off[b + 1];
+      ro[i] = off2[i];
+      off2[i + 1] = off2[i] + (bin_off[b + 1] - bin_off[b]);
+      win2[i] = bin_win[b];
+      list2[i] = i;
+    }
+    CK(ctx->rest_range.ensure(rr.size() * 8));
+    CK(ctx->rest_off.ensure(ro.size() * 8));
+    CK(ctx->rest_desc.ensure(std::max<uint64_t>(off2[R], 1) * 8));
+    CK(cudaMemcpyAsync(ctx->rest_range.p, rr.data(), rr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->rest_off.p, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    {
+      Timer tm(ctx, K_SHUFFLE);
+      CK(launch_gather_ranges(desc, ctx->rest_range.as<unsigned long long>(), ctx->rest_off.as<unsigned long long>(),
+                              R, ctx->rest_desc.as<uint64_t>(), ctx->sms, ctx->stream));
+    }
+    const double rho_before = ctx->rho;
+    st = count_waves_l2(ctx, stream_codes, ctx->rest_desc.as<uint64_t>(), off2, win2, list2, k, min_count,
+                        total_windows, pre);
+    if (st != GERBIL_OK) return st;
+    if (ctx->rho == rho_before && smem_obs > 0) ctx->rho = 0.0;  // no wave observation: use the smem one
+  }
+  if (smem_obs > 0) ctx->rho = std::min(1.0, std::max(ctx->rho, std::max(smem_obs * 1.15 + 0.01, 0.02)));
+  return st;
+}
+
 // ---------------------------------------------------------------------------
 // dfp(p) key table (reading Q23): sample m-mer
 // frequencies on the device (all ranks' samples summed), sort by (frequency,
@@ -777,7 +978,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   }
   // all ranks must agree on B: derive it from the largest local batch
   uint64_t nb_for_bins = n_bases;
-  const uint32_t B = choose_bins(ctx, nb_for_bins, W);
+  const uint32_t B = choose_bins(ctx, nb_for_bins, W, k, m);
   if (ctx->world > 1 && ctx->cfg.n_bins == 0)
     return fail(ctx, GERBIL_E_USAGE, "world > 1 requires an explicit n_bins (identical on all ranks)");
   CK(ctx->counters.ensure(sizeof(Counters)));

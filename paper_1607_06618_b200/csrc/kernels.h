@@ -129,6 +129,40 @@ struct CountArgs {
 };
 cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
 
+// count_smem.cu: steps (d)+(e) for bins whose distinct k-mers fit one warp's
+// shared-memory table (one warp per bin, warp-synchronous inserts, in-place
+// compaction). Abandoned bins (distinct > max_fill) are listed in `failed`.
+constexpr int kSmemMaxWarps = 16;
+constexpr int kRangeWinShift = 40;  // bin windows (clamped to 2^24 - 1) above the end descriptor index
+constexpr unsigned long long kRangeEndMask = (1ull << kRangeWinShift) - 1;
+struct SmemCountArgs {
+  const uint64_t* codes;             // stream the descriptors point into
+  const uint64_t* desc;              // bin-ordered descriptors
+  const unsigned long long* range;   // [n_list][2]: first descriptor; end descriptor | windows << kRangeWinShift
+  uint32_t n_list;
+  uint32_t k, min_count, canonical;
+  uint32_t cap;                      // table slots per warp (multiple of 32)
+  uint32_t max_fill;                 // abandon a bin past this many distinct k-mers (<= cap - 32)
+  uint64_t* out_keys;                // [out_cap * W]
+  uint32_t* out_counts;              // [out_cap]
+  uint64_t out_cap;
+  unsigned long long* out_n;
+  unsigned long long* sum_counts;
+  unsigned long long* distinct;
+  uint32_t* failed;                  // [n_list] list indices of abandoned bins
+  unsigned long long* n_failed;
+  uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 4 = no tag fast path
+};
+int smem_count_warps();                                      // warps per CTA (GERBIL_SMEM_WARPS, default 8)
+uint32_t smem_slot_bytes(uint32_t k);
+uint32_t smem_warp_bytes(uint32_t k, uint32_t cap);
+uint32_t smem_table_slots(uint32_t k, size_t smem_per_block);  // 0 = no room
+cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);
+// dst[dst_off[i] + j] = src[ranges[2i] + j] for j < ranges[2i+1] - ranges[2i]
+cudaError_t launch_gather_ranges(const uint64_t* src, const unsigned long long* ranges,
+                                 const unsigned long long* dst_off, uint32_t n, uint64_t* dst, int sms,
+                                 cudaStream_t s);
+
 struct CountKeysArgs {      // emergency path: insert overflow keys
   const uint64_t* keys;     // [n * W]
   uint64_t n;

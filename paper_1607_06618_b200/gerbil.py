@@ -22,6 +22,7 @@ _lib = C.CDLL(_LIB_PATH)
 OK, E_USAGE, E_IO, E_INTERNAL, E_NOMEM, E_CUDA, E_NCCL, E_STATE = range(8)
 FMT_BINARY, FMT_CSV = 0, 1
 ORDER_KMC2, ORDER_LEX, ORDER_CGAT, ORDER_ROBERTS, ORDER_RANDOM, ORDER_DFP = 0, 1, 2, 3, 4, 5
+COUNT_AUTO, COUNT_L2, COUNT_SMEM = 0, 1, 2  # gerbil_config.count_mode
 
 
 class GerbilError(RuntimeError):
@@ -52,6 +53,7 @@ class Config(C.Structure):
         ("disable_normalization", C.c_int32),
         ("dfp_pivot", C.c_double),
         ("order_sample_stride", C.c_uint32),
+        ("count_mode", C.c_int32),
     ]
 
 
@@ -98,6 +100,10 @@ class Stats(C.Structure):
         ("launches_count", C.c_uint32),
         ("launches_compact", C.c_uint32),
         ("launches_total", C.c_uint32),
+        ("smem_bins", C.c_uint64),
+        ("smem_failed", C.c_uint64),
+        ("smem_windows", C.c_uint64),
+        ("smem_slots", C.c_uint32),
     ]
 
     def as_dict(self) -> dict:
@@ -223,7 +229,7 @@ class Gerbil:
                  max_probes: int = 0, distinct_ratio: float = 0.0, target_load: float = 0.0,
                  wave_table_bytes: int = 0, host_threads: int = 0, stream: int | None = None,
                  timing: bool = False, force_exchange: bool = False, canonical: bool = True,
-                 dfp_pivot: float = 0.5, order_sample_stride: int = 0):
+                 dfp_pivot: float = 0.5, order_sample_stride: int = 0, count_mode: int = 0):
         cfg = Config()
         _lib.gerbil_config_default(C.byref(cfg))
         cfg.device = device
@@ -245,6 +251,7 @@ class Gerbil:
         cfg.disable_normalization = 0 if canonical else 1
         cfg.dfp_pivot = dfp_pivot
         cfg.order_sample_stride = order_sample_stride
+        cfg.count_mode = count_mode
         h = C.c_void_p()
         st = _lib.gerbil_init(C.byref(cfg), C.byref(h))
         if st != OK:
