@@ -168,6 +168,27 @@ struct SpillState {
   }
 };
 
+// Page-locked host staging buffer (grown on demand): per-bin tables of 10^6 bins move
+// at PCIe speed instead of through pageable bounce buffers.
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    const size_t want = std::max<size_t>(n + n / 8, 4096);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
 struct Wave {
   uint64_t d0, d1;   // descriptor range (bin-ordered)
   uint64_t windows;
@@ -204,6 +225,7 @@ struct gerbil_ctx {
   DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
   DevBuf smem_range, smem_failed, rest_desc, rest_range, rest_off;  // step (d) in shared memory
   int smem_optin = 0;  // max dynamic shared memory per block (bytes)
+  PinnedBuf h_hist, h_rng;  // per-bin histogram download, shared-memory bin list upload
   Counters* h_counters = nullptr;  // pinned
   // results
   bool have_result = false;
@@ -685,7 +707,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   ctx->stats.smem_slots = cap;
   if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
                                       total_windows, Preset{});
-  const uint32_t max_fill = cap - std::max<uint32_t>(32u, cap / 4);
+  const uint32_t max_fill = cap - std::max<uint32_t>(64u, cap / 4);  // a round inserts <= 64
   const bool force = ctx->cfg.count_mode == 2;
   std::vector<uint32_t> elig, rest;
   for (uint32_t b : bins) {
@@ -698,10 +720,12 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   if (elig.empty())
     return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count, total_windows,
                           Preset{});
-  // heaviest first: the static round-robin gives every warp a similar mix
-  std::stable_sort(elig.begin(), elig.end(), [&](uint32_t a, uint32_t b) { return bin_win[a] > bin_win[b]; });
+  // bin order: bins are hashes of minimizers, so a static round-robin over them already
+  // gives every warp a similar mix of sizes
+  trace("smem bins selected");
   const uint32_t n = (uint32_t)elig.size();
-  std::vector<unsigned long long> rng(2 * (size_t)n);
+  CK(ctx->h_rng.ensure(2 * (size_t)n * 8));
+  unsigned long long* rng = ctx->h_rng.as<unsigned long long>();
   uint64_t out_bound = 0, elig_windows = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t b = elig[i];
@@ -710,12 +734,12 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     out_bound += std::min<uint64_t>(bin_win[b], max_fill);
     elig_windows += bin_win[b];
   }
-  CK(ctx->smem_range.ensure(rng.size() * 8));
+  CK(ctx->smem_range.ensure(2 * (size_t)n * 8));
   CK(ctx->smem_failed.ensure((size_t)n * 4 + 8));
   CK(ctx->out_keys.ensure(std::max<uint64_t>(out_bound, 1) * W * 8));
   CK(ctx->out_counts.ensure(std::max<uint64_t>(out_bound, 1) * 4));
   CK(ctx->counters.ensure(sizeof(Counters)));
-  CK(cudaMemcpyAsync(ctx->smem_range.p, rng.data(), rng.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->smem_range.p, rng, 2 * (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
   Counters* dc = ctx->counters.as<Counters>();
   CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
   CK(cudaMemsetAsync(&dc->read_work, 0, 8, ctx->stream));  // n_failed
@@ -741,6 +765,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     Timer tm(ctx, K_COUNT);
     CK(launch_count_smem(a, ctx->sms, ctx->stream));
   }
+  trace("smem count issued");
   Counters& hc = *ctx->h_counters;
   CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -760,6 +785,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     rest.push_back(elig[li]);
     failed_windows += bin_win[elig[li]];
   }
+  trace("smem count done (synced)");
   ctx->stats.smem_bins += n;
   ctx->stats.smem_failed += n_failed;
   const uint64_t smem_windows = elig_windows - failed_windows;
@@ -996,12 +1022,15 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   const uint64_t local_windows = ctx->h_counters->n_windows;
   ctx->stats.supermers = n_sm;
   ctx->stats.valid_windows = local_windows;
-  std::vector<unsigned long long> hist(3ull * B);
-  CK(cudaMemcpyAsync(hist.data(), ctx->hist.p, 3ull * B * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx->h_hist.ensure(3ull * B * 8));
+  const unsigned long long* hist = ctx->h_hist.as<unsigned long long>();
+  CK(cudaMemcpyAsync(ctx->h_hist.p, ctx->hist.p, 3ull * B * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  trace("histogram downloaded");
 
   std::vector<uint64_t> bin_win(B), bin_off(B + 1, 0);
   std::vector<uint32_t> owned;
+  owned.reserve(B);
   const uint64_t* stream_codes = codes;
   uint64_t owned_windows = 0;
   if (!ctx->comm) {

@@ -117,18 +117,31 @@ __device__ __forceinline__ void extract_stage(const uint64_t* s, uint32_t o, uin
   if (tail < 64) x[W - 1] &= ~0ull << (64 - tail);
 }
 
-// Same without bounds checks: words past the k-mer may be read (they stay inside the
-// warp's shared memory: rc stage, map and table follow the stages) but only feed bits
-// that the tail mask clears. (a >> 1) >> (63 - sh) is a >> (64 - sh) without the sh = 0 case.
+// Same without bounds checks, from 32-bit funnel shifts: words past the k-mer may be
+// read (they stay inside the warp's shared memory: rc stage, map and table follow the
+// stages) but only feed bits that the tail mask clears. The stream's 32-bit units in
+// order are hi(w0), lo(w0), hi(w1), ...; the k-mer starts in unit 2*(o/32) + (o%32)/16.
 template <int W>
 __device__ __forceinline__ void extract_fast(const uint64_t* s, uint32_t o, uint64_t tmask, uint64_t (&x)[W]) {
   const uint64_t* p = s + (o >> 5);
-  const uint32_t sh = (o & 31) * 2;
-  uint64_t a[W + 1];
+  const bool odd = (o & 16u) != 0;   // starts in the low half of word o/32
+  const uint32_t r = (o & 15u) * 2;  // bit shift inside the 32-bit unit
+  uint32_t u[2 * W + 2];
 #pragma unroll
-  for (int i = 0; i <= W; ++i) a[i] = p[i];
+  for (int i = 0; i <= W; ++i) {
+    const uint64_t a = p[i];
+    u[2 * i] = (uint32_t)(a >> 32);
+    u[2 * i + 1] = (uint32_t)a;
+  }
+  uint32_t v[2 * W + 1];
 #pragma unroll
-  for (int i = 0; i < W; ++i) x[i] = (a[i] << sh) | ((a[i + 1] >> 1) >> (63 - sh));
+  for (int n = 0; n <= 2 * W; ++n) v[n] = odd ? u[n + 1] : u[n];
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const uint32_t hi = __funnelshift_l(v[2 * i + 1], v[2 * i], r);
+    const uint32_t lo = __funnelshift_l(v[2 * i + 2], v[2 * i + 1], r);
+    x[i] = ((uint64_t)hi << 32) | lo;
+  }
   x[W - 1] &= tmask;
 }
 

@@ -142,7 +142,7 @@ struct SmemCountArgs {
   uint32_t n_list;
   uint32_t k, min_count, canonical;
   uint32_t cap;                      // table slots per warp (multiple of 32)
-  uint32_t max_fill;                 // abandon a bin past this many distinct k-mers (<= cap - 32)
+  uint32_t max_fill;                 // abandon a bin past this many distinct k-mers (<= cap - 64)
   uint64_t* out_keys;                // [out_cap * W]
   uint32_t* out_counts;              // [out_cap]
   uint64_t out_cap;

@@ -176,7 +176,7 @@ def test_overflow_path_exact(G, k):
     ref = oracle.count(text, k)
     # θ = 1 bucket and an over-full table: many k-mers take the emergency path
     keys, counts, st = _gpu_count_text(G, text, k, 9, 1, max_probes=1, target_load=1.6,
-                                       distinct_ratio=0.3, n_bins=4)
+                                       distinct_ratio=0.3, n_bins=4, count_mode=G.COUNT_L2)
     compare(keys, counts, k, ref)
     assert st["overflow_kmers"] > 0 and st["overflow_passes"] == 1
 
@@ -186,7 +186,8 @@ def test_recount_when_emergency_area_exhausted(G):
     text = synth.fastx(w, synth.FASTQ)
     ref = oracle.count(text, 40)
     # ρ̂ far too small: overflow exceeds the emergency area → waves are recounted
-    keys, counts, st = _gpu_count_text(G, text, 40, 7, 1, distinct_ratio=0.001, max_probes=2)
+    keys, counts, st = _gpu_count_text(G, text, 40, 7, 1, distinct_ratio=0.001, max_probes=2,
+                                       count_mode=G.COUNT_L2)
     compare(keys, counts, 40, ref)
     assert st["ratio_used"] > 0.001
 
