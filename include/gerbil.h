@@ -305,6 +305,26 @@ gerbil_status gerbil_results_device(gerbil_ctx* ctx, const uint64_t** d_kmers,
                                     const uint32_t** d_counts, uint64_t* n,
                                     uint32_t* W);
 
+/* Step (c) exchange plan (host only, no device needed): what every rank computes,
+ * identically, from the all-gathered per-bin histograms before the NCCL
+ * all-to-all (PAPER.md:49 — all occurrences of a k-mer go to one temporary
+ * file, here one owner rank; the LPT ownership replaces the paper's load
+ * balancer).
+ *   hist:  [world][3][n_bins] u64, rank-major: windows, super-mers and payload
+ *          words of every bin produced by step (b) on that rank (input, not retained).
+ *   owner: [n_bins] out — owner rank of each bin: bins sorted by total windows
+ *          (heaviest first, ties by bin index) go to the least-loaded rank (ties
+ *          by rank index), so every rank derives the same map.
+ *   send_desc_off, send_word_off: [world + 1] out — this rank's send buffer
+ *          layout: descriptors / payload words for destination d occupy
+ *          [off[d], off[d+1]), bins in increasing order inside a destination.
+ *   recv_desc_off, recv_word_off: [world + 1] out — receive layout by source.
+ * GERBIL_E_USAGE on a NULL pointer, world < 1, rank outside [0, world) or
+ * n_bins == 0. */
+gerbil_status gerbil_exchange_plan(const uint64_t* hist, uint32_t n_bins, int32_t world, int32_t rank,
+                                   int32_t* owner, uint64_t* send_desc_off, uint64_t* send_word_off,
+                                   uint64_t* recv_desc_off, uint64_t* recv_word_off);
+
 gerbil_status gerbil_get_stats(const gerbil_ctx* ctx, gerbil_stats* out);
 const char* gerbil_last_error(const gerbil_ctx* ctx);
 void gerbil_finalize(gerbil_ctx* ctx);

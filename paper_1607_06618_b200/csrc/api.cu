@@ -351,6 +351,50 @@ uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, 
   return B;
 }
 
+// Step (c) plan from the all-gathered histograms H[world][3][B] (windows, super-mers,
+// payload words): LPT bin owners (heaviest bin first to the least-loaded rank; ties to
+// the lower bin / rank, so every rank derives the same map), this rank's send layout
+// by destination and receive layout by source (inside each, owned bins in bin order).
+void exchange_plan(const uint64_t* H, uint32_t B, int P, int r, int32_t* owner, uint64_t* sd_off,
+                   uint64_t* sw_off, uint64_t* rd_off, uint64_t* rw_off) {
+  auto Hw = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + b]; };
+  auto Hc = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + B + b]; };
+  auto Hp = [&](int s, uint32_t b) { return H[(size_t)s * 3 * B + 2 * B + b]; };
+  std::vector<uint64_t> gw(B, 0);
+  for (int s = 0; s < P; ++s)
+    for (uint32_t b = 0; b < B; ++b) gw[b] += Hw(s, b);
+  std::vector<uint32_t> order(B);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return gw[a] > gw[b]; });
+  std::vector<uint64_t> load(P, 0);
+  for (uint32_t b : order) {
+    int best = 0;
+    for (int p = 1; p < P; ++p)
+      if (load[p] < load[best]) best = p;
+    owner[b] = best;
+    load[best] += gw[b];
+  }
+  for (int i = 0; i <= P; ++i) sd_off[i] = sw_off[i] = rd_off[i] = rw_off[i] = 0;
+  for (uint32_t b = 0; b < B; ++b) {
+    sd_off[owner[b] + 1] += Hc(r, b);
+    sw_off[owner[b] + 1] += Hp(r, b);
+  }
+  for (int d = 0; d < P; ++d) {
+    sd_off[d + 1] += sd_off[d];
+    sw_off[d + 1] += sw_off[d];
+  }
+  for (int s = 0; s < P; ++s) {
+    uint64_t cd = 0, cw = 0;
+    for (uint32_t b = 0; b < B; ++b)
+      if (owner[b] == r) {
+        cd += Hc(s, b);
+        cw += Hp(s, b);
+      }
+    rd_off[s + 1] = rd_off[s] + cd;
+    rw_off[s + 1] = rw_off[s] + cw;
+  }
+}
+
 double wall_ms() {
   return std::chrono::duration<double, std::milli>(
              std::chrono::steady_clock::now().time_since_epoch())
@@ -1072,46 +1116,23 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
     for (int s = 0; s < P; ++s)
       for (uint32_t b = 0; b < B; ++b) gw[b] += Hw(s, b);
     ctx->stats.max_bin_windows = *std::max_element(gw.begin(), gw.end());
-    // LPT: heaviest bin first to the least-loaded rank (ties → lower rank/bin)
-    std::vector<uint32_t> order(B);
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return gw[a] > gw[b]; });
-    std::vector<int> owner(B);
-    std::vector<uint64_t> load(P, 0);
-    for (uint32_t b : order) {
-      int best = 0;
-      for (int p = 1; p < P; ++p)
-        if (load[p] < load[best]) best = p;
-      owner[b] = best;
-      load[best] += gw[b];
-    }
-    // send layout ordered by (dest, bin)
-    std::vector<uint64_t> sd_off(P + 1, 0), sw_off(P + 1, 0);
+    // LPT owners and the send / receive layouts (exchange_plan, also gerbil_exchange_plan)
+    std::vector<int32_t> owner(B);
+    std::vector<uint64_t> sd_off(P + 1, 0), sw_off(P + 1, 0), rd_off(P + 1, 0), rw_off(P + 1, 0);
+    exchange_plan(reinterpret_cast<const uint64_t*>(H.data()), B, P, r, owner.data(), sd_off.data(),
+                  sw_off.data(), rd_off.data(), rw_off.data());
+    // per-bin send cursors: inside a destination's range, bins in increasing order
     std::vector<unsigned long long> cur_d(B), cur_w(B), seg(B);
-    for (int d = 0; d < P; ++d) {
-      uint64_t cd = sd_off[d], cw = sw_off[d];
-      for (uint32_t b = 0; b < B; ++b)
-        if (owner[b] == d) {
-          cur_d[b] = cd;
-          cur_w[b] = cw;
-          seg[b] = sw_off[d];
-          cd += Hc(r, b);
-          cw += Hp(r, b);
-        }
-      sd_off[d + 1] = cd;
-      sw_off[d + 1] = cw;
-    }
-    // receive layout: source-major; inside a source, owned bins in bin order
-    std::vector<uint64_t> rd_off(P + 1, 0), rw_off(P + 1, 0);
-    for (int s = 0; s < P; ++s) {
-      uint64_t cd = 0, cw = 0;
-      for (uint32_t b = 0; b < B; ++b)
-        if (owner[b] == r) {
-          cd += Hc(s, b);
-          cw += Hp(s, b);
-        }
-      rd_off[s + 1] = rd_off[s] + cd;
-      rw_off[s + 1] = rw_off[s] + cw;
+    {
+      std::vector<uint64_t> cd(sd_off.begin(), sd_off.end() - 1), cw(sw_off.begin(), sw_off.end() - 1);
+      for (uint32_t b = 0; b < B; ++b) {
+        const int d = owner[b];
+        cur_d[b] = cd[d];
+        cur_w[b] = cw[d];
+        seg[b] = sw_off[d];
+        cd[d] += Hc(r, b);
+        cw[d] += Hp(r, b);
+      }
     }
     const uint64_t n_send = sd_off[P], w_send = sw_off[P], n_recv = rd_off[P], w_recv = rw_off[P];
     CK(ctx->send_desc.ensure(std::max<uint64_t>(n_send, 1) * 8));
@@ -1339,6 +1360,20 @@ void gerbil_finalize(gerbil_ctx* ctx) {
 }
 
 const char* gerbil_last_error(const gerbil_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+gerbil_status gerbil_exchange_plan(const uint64_t* hist, uint32_t n_bins, int32_t world, int32_t rank,
+                                   int32_t* owner, uint64_t* send_desc_off, uint64_t* send_word_off,
+                                   uint64_t* recv_desc_off, uint64_t* recv_word_off) {
+  if (!hist || !owner || !send_desc_off || !send_word_off || !recv_desc_off || !recv_word_off || world < 1 ||
+      rank < 0 || rank >= world || n_bins == 0)
+    return GERBIL_E_USAGE;
+  try {
+    exchange_plan(hist, n_bins, world, rank, owner, send_desc_off, send_word_off, recv_desc_off, recv_word_off);
+  } catch (...) {
+    return GERBIL_E_NOMEM;
+  }
+  return GERBIL_OK;
+}
 
 gerbil_status gerbil_get_stats(const gerbil_ctx* ctx, gerbil_stats* out) {
   if (!ctx || !out) return GERBIL_E_USAGE;

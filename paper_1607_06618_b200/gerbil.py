@@ -113,6 +113,8 @@ class Stats(C.Structure):
 _P = C.c_void_p
 _U64P = C.POINTER(C.c_uint64)
 _lib.gerbil_config_default.argtypes = [C.POINTER(Config)]
+_lib.gerbil_exchange_plan.argtypes = [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]
 _lib.gerbil_init.argtypes = [C.POINTER(Config), C.POINTER(_P)]
 _lib.gerbil_nccl_unique_id.argtypes = [_P, C.c_size_t]
 _lib.gerbil_count.argtypes = [_P, C.POINTER(Reads), C.c_uint32, C.c_uint32, C.c_uint32]
@@ -141,7 +143,8 @@ for _f in ("gerbil_init", "gerbil_nccl_unique_id", "gerbil_count", "gerbil_count
            "gerbil_count_host_packed", "gerbil_count_host_stream", "gerbil_minimizer_stats", "gerbil_pack_reads",
            "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish", "gerbil_parse_text",
            "gerbil_count_text", "gerbil_fetch", "gerbil_results_device",
-           "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results"):
+           "gerbil_get_stats", "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
+           "gerbil_exchange_plan"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTED = [
@@ -150,7 +153,7 @@ EXPORTED = [
     "gerbil_fetch", "gerbil_minimizer_stats", "gerbil_spill_begin", "gerbil_spill_add", "gerbil_spill_finish",
     "gerbil_parse_text", "gerbil_count_text",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
-    "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results",
+    "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results", "gerbil_exchange_plan",
 ]
 
 
@@ -176,6 +179,29 @@ def nccl_unique_id() -> bytes:
     if st != OK:
         raise GerbilError(st, "ncclGetUniqueId failed")
     return buf.raw
+
+
+@dataclass
+class ExchangePlan:
+    owner: np.ndarray          # [n_bins] int32 owner rank of each bin
+    send_desc_off: np.ndarray  # [world + 1] this rank's send layout (descriptors) by destination
+    send_word_off: np.ndarray  # [world + 1] ... (payload words)
+    recv_desc_off: np.ndarray  # [world + 1] receive layout by source
+    recv_word_off: np.ndarray
+
+
+def exchange_plan(hist: np.ndarray, rank: int) -> ExchangePlan:
+    """Step (c) plan (host only): hist[world, 3, n_bins] u64 = per-rank windows, super-mers and
+    payload words of every bin (the all-gathered step-(b) histograms)."""
+    h = np.ascontiguousarray(hist, dtype=np.uint64)
+    world, three, n_bins = h.shape
+    assert three == 3
+    owner = np.zeros(n_bins, np.int32)
+    offs = [np.zeros(world + 1, np.uint64) for _ in range(4)]
+    st = _lib.gerbil_exchange_plan(_ptr(h), n_bins, world, rank, _ptr(owner), *(_ptr(o) for o in offs))
+    if st != OK:
+        raise GerbilError(st, "gerbil_exchange_plan failed")
+    return ExchangePlan(owner, *offs)
 
 
 @dataclass
