@@ -4,7 +4,8 @@ A step = one pass of the whole hot path (b) minimizer/super-mer/bin → (c) bin
 shuffle → (d) per-bin counting → (e) min-count compaction, over one batch of
 synthetic reads already resident in HBM, through the C ABI
 (gerbil_count_device). N=1 workload = BASELINE.json configs[1]: F. vesca-scale
-synthetic Illumina reads (5×10^7 × 100 bp = 5 Gbp), k=40, m=7, min_count=1.
+synthetic Illumina reads (5×10^7 × 100 bp = 5 Gbp), k=40, min_count=1; m=15 (results do
+not depend on m; m=15 makes ~4M bins small enough for the shared-memory count kernel).
 Under torchrun (N>1) every rank counts its own 5 Gbp shard (weak scaling) and
 bins are shuffled across ranks with NCCL.
 
@@ -32,7 +33,7 @@ UNIT = "bases/s"
 
 # configs[1]: "F. vesca-scale synthetic Illumina reads (~5 Gbp, 100-bp), k=40, 1xB200"
 C1 = dict(seed=2, genome_len=240_000_000, read_len=100, n_reads=50_000_000, err=0.0033, nrate=0.0001)
-K, M, MIN_COUNT = 40, 7, 1
+K, M, MIN_COUNT = 40, 15, 1
 WORKLOAD_NAME = ""
 
 
@@ -232,7 +233,8 @@ def main() -> None:
     sampler = ClockSampler(local)
     sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    per_kernel = {"count": [0.0, 0], "compact": [0.0, 0], "supermer": [0.0, 0], "shuffle": [0.0, 0]}
+    per_kernel = {"count": [0.0, 0], "compact": [0.0, 0], "supermer": [0.0, 0], "shuffle": [0.0, 0],
+                  "smem": [0.0, 0]}
     launches = 0
     if world > 1:
         dist.barrier()
@@ -247,6 +249,8 @@ def main() -> None:
         per_kernel["compact"][1] += st["launches_compact"]
         per_kernel["supermer"][0] += st["ms_supermer"]
         per_kernel["shuffle"][0] += st["ms_shuffle"]
+        per_kernel["smem"][0] += st["ms_smem"]
+        per_kernel["smem"][1] += st["launches_smem"]
         launches += st["launches_total"]
     ev1.record(stream)
     torch.cuda.synchronize(dev)
@@ -270,49 +274,76 @@ def main() -> None:
     # ---- roofline of the dominant kernel (count, step d) ----------------------------------
     peak, peak_src = _peaks()
     W = st["W"]
-    # table bytes per slot: 16 B inline slots for k <= 46, else the chunked bucket / 4
-    slot = 16 if K <= 46 else (32 + 32 * ((K + 30) // 31)) / 4
-    n_count = max(per_kernel["count"][1], 1)
-    avg_count_ms = per_kernel["count"][0] / n_count
-    # algorithmic bytes per step of the count kernel (SURVEY.md §8(d) stream model restricted to
-    # this kernel): descriptors (8 B/super-mer), packed super-mer bases
-    # (0.25 B/base), and one write of every claimed table slot (slot B per distinct k-mer).
     sm_bases = st["valid_windows"] + st["supermers"] * (K - 1)
-    count_bytes_step = 8 * st["supermers"] + 0.25 * sm_bases + slot * st["distinct"]
-    bytes_per_launch = count_bytes_step / max(st["launches_count"], 1)
-    achieved = bytes_per_launch / (avg_count_ms / 1e3) / 1e9 if avg_count_ms > 0 else None
-    # ncu-measured DRAM bytes per launch of this kernel (profiles/, same workload): traffic
-    traffic = None
+    traffic_tbl = {}
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
-        if tj.get("workload") == WORKLOAD_NAME and tj.get("kernel") == "count_inline_kernel":
-            traffic = tj.get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "kernel": "count_inline_kernel<2,true>", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "peak_source": peak_src,
-                "bytes_model": f"8*supermers + 0.25*supermer_bases + {slot:g}*distinct per step",
-                "algorithmic_bytes_per_launch": bytes_per_launch,
-                "avg_launch_ms": avg_count_ms, "launches_per_step": st["launches_count"],
-                "share_of_step": per_kernel["count"][0] / args.steps / ms,
-                "note": "L2-resident table: the kernel is bound by the L2 random-access rate of its "
-                        "bucket-load + atomic pattern, not HBM; see l2_ceiling and DESIGN.md §4"}
-    # The bound that applies: one 64-byte bucket load + one atomic into the same bucket per window
-    # (RED for a k-mer already present, 128-bit CAS for a new one). scripts/l2_micro.cu measured what
-    # B200's L2 sustains for exactly these patterns on a 64 MiB table (profiles/r01_l2_micro.txt).
-    L2_LOAD_RED, L2_LOAD_CAS = 49.2e9, 38.3e9  # ops/s, "load+red" / "load+cas" rows
-    new_k = float(st["distinct"])
-    hits = max(float(st["valid_windows"]) - new_k, 0.0)
-    t_floor = hits / L2_LOAD_RED + new_k / L2_LOAD_CAS
-    d_ms = per_kernel["count"][0] / args.steps  # steps (d)+(e) device time per step
-    l2_ceiling = {"bound": "l2_random_ops", "unit": "G window-ops/s",
-                  "achieved": float(st["valid_windows"]) / (d_ms / 1e3) / 1e9 if d_ms > 0 else None,
-                  "peak": float(st["valid_windows"]) / t_floor / 1e9 if t_floor > 0 else None,
-                  "frac": (t_floor * 1e3 / d_ms) if d_ms > 0 else None,
-                  "floor_ms": t_floor * 1e3, "measured_ms": d_ms,
-                  "source": "profiles/r01_l2_micro.txt (load+red 49.2, load+cas 38.3 Gop/s, 64 MiB table); "
-                            "measured_ms = steps (d)+(e) incl. compaction"}
-    roofline["l2_ceiling"] = l2_ceiling
+        for e in (tj if isinstance(tj, list) else [tj]):
+            if e.get("workload") == WORKLOAD_NAME:
+                traffic_tbl[e.get("kernel")] = e
+    smem_share = st["smem_windows"] / max(st["valid_windows"], 1)
+    if smem_share >= 0.5:
+        # step (d)+(e) in per-warp shared-memory tables (count_smem.cu): per window, the
+        # algorithmic HBM bytes are the descriptor (8 B/super-mer) and packed bases (0.25 B/base)
+        # it reads and the (8W+4)-byte (k-mer, count) pair it writes per kept k-mer; the table
+        # lives in shared memory. Units per launch = the windows it counted.
+        n_smem = max(per_kernel["smem"][1], 1)
+        avg_ms = per_kernel["smem"][0] / n_smem
+        per_window = (8 * st["supermers"] + 0.25 * sm_bases + (8 * W + 4) * st["kept"]) / max(st["valid_windows"], 1)
+        bytes_per_launch = per_window * st["smem_windows"] / max(st["launches_smem"], 1)
+        achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else None
+        kname = "count_smem_kernel<2,true>"
+        tr = traffic_tbl.get("count_smem_kernel", {})
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": tr.get("dram_bytes_per_launch"), "peak_source": peak_src,
+                    "bytes_model": f"per window: (8*supermers + 0.25*supermer_bases + {8 * W + 4}*kept) / windows; "
+                                   "x windows counted in shared memory per launch",
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                    "launches_per_step": st["launches_smem"],
+                    "share_of_step": per_kernel["smem"][0] / args.steps / ms,
+                    "windows_share": smem_share,
+                    "issue_slot_util": tr.get("issue_slots_busy"),
+                    "note": "table in shared memory: the kernel is bound by instruction issue and "
+                            "shared-memory latency (ncu issue_slot_util), not HBM; DESIGN.md §4"}
+    else:
+        # table bytes per slot: 16 B inline slots for k <= 46, else the chunked bucket / 4
+        slot = 16 if K <= 46 else (32 + 32 * ((K + 30) // 31)) / 4
+        n_count = max(per_kernel["count"][1], 1)
+        avg_count_ms = per_kernel["count"][0] / n_count
+        # algorithmic bytes per step of the count kernel (SURVEY.md §8(d) stream model restricted to
+        # this kernel): descriptors (8 B/super-mer), packed super-mer bases
+        # (0.25 B/base), and one write of every claimed table slot (slot B per distinct k-mer).
+        count_bytes_step = 8 * st["supermers"] + 0.25 * sm_bases + slot * st["distinct"]
+        bytes_per_launch = count_bytes_step / max(st["launches_count"], 1)
+        achieved = bytes_per_launch / (avg_count_ms / 1e3) / 1e9 if avg_count_ms > 0 else None
+        tr = traffic_tbl.get("count_inline_kernel", {})
+        roofline = {"bound": "hbm", "kernel": "count_inline_kernel<2,true>", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                    "traffic": tr.get("dram_bytes_per_launch"), "peak_source": peak_src,
+                    "bytes_model": f"8*supermers + 0.25*supermer_bases + {slot:g}*distinct per step",
+                    "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "avg_launch_ms": avg_count_ms, "launches_per_step": st["launches_count"],
+                    "share_of_step": per_kernel["count"][0] / args.steps / ms,
+                    "note": "L2-resident table: the kernel is bound by the L2 random-access rate of its "
+                            "bucket-load + atomic pattern, not HBM; see l2_ceiling and DESIGN.md §4"}
+        # The bound that applies: one 64-byte bucket load + one atomic into the same bucket per window
+        # (RED for a k-mer already present, 128-bit CAS for a new one). scripts/l2_micro.cu measured
+        # what B200's L2 sustains for these patterns on a 64 MiB table (profiles/r01_l2_micro.txt).
+        L2_LOAD_RED, L2_LOAD_CAS = 49.2e9, 38.3e9  # ops/s, "load+red" / "load+cas" rows
+        new_k = float(st["distinct"])
+        hits = max(float(st["valid_windows"]) - new_k, 0.0)
+        t_floor = hits / L2_LOAD_RED + new_k / L2_LOAD_CAS
+        d_ms = per_kernel["count"][0] / args.steps  # steps (d)+(e) device time per step
+        roofline["l2_ceiling"] = {
+            "bound": "l2_random_ops", "unit": "G window-ops/s",
+            "achieved": float(st["valid_windows"]) / (d_ms / 1e3) / 1e9 if d_ms > 0 else None,
+            "peak": float(st["valid_windows"]) / t_floor / 1e9 if t_floor > 0 else None,
+            "frac": (t_floor * 1e3 / d_ms) if d_ms > 0 else None,
+            "floor_ms": t_floor * 1e3, "measured_ms": d_ms,
+            "source": "profiles/r01_l2_micro.txt (load+red 49.2, load+cas 38.3 Gop/s, 64 MiB table); "
+                      "measured_ms = steps (d)+(e) incl. compaction"}
 
     # ---- end to end through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -368,6 +399,7 @@ def main() -> None:
             "stage_ms": {"supermer": per_kernel["supermer"][0] / args.steps,
                          "shuffle": per_kernel["shuffle"][0] / args.steps,
                          "count": per_kernel["count"][0] / args.steps,
+                         "count_smem_kernel": per_kernel["smem"][0] / args.steps,
                          "compact": per_kernel["compact"][0] / args.steps},
             "result": {"distinct": st["distinct"], "kept": st["kept"], "supermers": st["supermers"],
                        "valid_windows": st["valid_windows"], "ratio_observed": st["ratio_observed"],

@@ -168,6 +168,8 @@ typedef struct {
   uint64_t smem_failed;      /* of which abandoned (too many distinct k-mers) and recounted in L2 */
   uint64_t smem_windows;     /* windows of the bins that completed in shared memory */
   uint32_t smem_slots;       /* table slots per warp */
+  uint32_t launches_smem;    /* shared-memory count launches (included in launches_count) */
+  double ms_smem;            /* their device time (included in ms_count) */
 } gerbil_stats;
 
 /* Fills cfg with defaults (struct_size set, everything else "auto"). */

@@ -83,7 +83,7 @@ bool use_reads_kernel(uint32_t k, uint32_t m, uint64_t n_bases, uint64_t n_reads
   return false;
 }
 
-enum Kind { K_SUPERMER, K_SHUFFLE, K_COUNT, K_COMPACT, K_OVERFLOW, K_H2D, K_NKIND };
+enum Kind { K_SUPERMER, K_SHUFFLE, K_COUNT, K_COMPACT, K_OVERFLOW, K_H2D, K_SMEM, K_NKIND };
 
 struct TimedEvent {
   int kind;
@@ -226,6 +226,7 @@ struct gerbil_ctx {
   DevBuf smem_range, smem_failed, rest_desc, rest_range, rest_off;  // step (d) in shared memory
   int smem_optin = 0;  // max dynamic shared memory per block (bytes)
   PinnedBuf h_hist, h_rng;  // per-bin histogram download, shared-memory bin list upload
+  DevBuf bin_off_d, plan_sums;  // device-side bin plan (many bins, one rank)
   Counters* h_counters = nullptr;  // pinned
   // results
   bool have_result = false;
@@ -324,6 +325,10 @@ gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_co
 }
 
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k);
+// from this many bins up, a single rank plans steps (c)-(e) on the device
+constexpr uint32_t kDevicePlanBins = 1u << 16;
+gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
+                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows);
 
 uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, uint32_t m) {
   if (ctx->cfg.n_bins) return ctx->cfg.n_bins;
@@ -335,7 +340,7 @@ uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, 
   if (cap) {
     const double want = ctx->rho * (double)n_bases * ctx->world / (0.35 * cap);
     uint32_t B = 512;
-    while ((double)B < want && B < (1u << 20)) B <<= 1;
+    while ((double)B < want && B < (1u << 22)) B <<= 1;
     while (B < 64u * (uint32_t)ctx->world) B <<= 1;
     return B;
   }
@@ -737,56 +742,37 @@ uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
   return cap >= 128 ? cap : 0;
 }
 
-// Steps (d)+(e) over the bin-ordered descriptors of this rank. Bins predicted
-// (ρ̂ · windows) to fit one warp's shared-memory table are counted there, in
-// one launch (count_smem.cu); the others — and any bin the shared-memory pass
-// abandoned — are gathered into one contiguous descriptor range and counted in
-// the L2-resident wave tables, whose results are appended.
-gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
-                          const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
-                          const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
-                          uint64_t total_windows) {
+// Abandonment threshold of the shared-memory tables: a round inserts <= 32 k-mers, so
+// a table never fills.
+uint32_t smem_max_fill(uint32_t cap) { return cap - std::max<uint32_t>(64u, cap / 4); }
+
+// Windows up to which a bin goes to the shared-memory pass: predicted distinct
+// (ρ̂ · windows) within the abandonment threshold; a miss costs only the bin's
+// partial work (it is recounted in the wave tables). count_mode 2: every bin.
+uint64_t smem_window_threshold(const gerbil_ctx* ctx, uint32_t max_fill) {
+  if (ctx->cfg.count_mode == 2) return ~0ull;
+  return std::max<uint64_t>(max_fill, (uint64_t)(0.95 * max_fill / std::max(ctx->rho, 1e-6)));
+}
+
+struct RestBin {
+  uint64_t d0, d1, win;  // descriptor range and windows of a bin for the L2 wave tables
+};
+
+// Steps (d)+(e): the shared-memory pass over the n bins listed (device) in
+// ctx->smem_range, then the bins of `rest` plus every bin the shared-memory pass
+// abandoned, gathered into one contiguous descriptor range and counted in the
+// L2-resident wave tables, whose results are appended.
+gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc, uint32_t n,
+                                 uint64_t elig_windows, uint64_t out_bound, uint32_t cap, uint32_t max_fill,
+                                 std::vector<RestBin>& rest, uint32_t k, uint32_t min_count,
+                                 uint64_t total_windows) {
   const uint32_t W = key_words(k);
-  const uint32_t cap = ctx->rec_out ? 0u : smem_slots_for(ctx, k);
-  ctx->stats.smem_slots = cap;
-  if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
-                                      total_windows, Preset{});
-  const uint32_t max_fill = cap - std::max<uint32_t>(64u, cap / 4);  // a round inserts <= 64
-  const bool force = ctx->cfg.count_mode == 2;
-  std::vector<uint32_t> elig, rest;
-  for (uint32_t b : bins) {
-    if (bin_off[b + 1] == bin_off[b]) continue;  // no super-mers, nothing to count
-    // predicted distinct (ρ̂ · windows) within the abandonment threshold; a miss costs
-    // only the bin's partial work (it is recounted in the wave tables)
-    const bool fits = bin_win[b] <= max_fill || ctx->rho * (double)bin_win[b] <= 0.95 * max_fill;
-    (force || fits ? elig : rest).push_back(b);
-  }
-  if (elig.empty())
-    return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count, total_windows,
-                          Preset{});
-  // bin order: bins are hashes of minimizers, so a static round-robin over them already
-  // gives every warp a similar mix of sizes
-  trace("smem bins selected");
-  const uint32_t n = (uint32_t)elig.size();
-  CK(ctx->h_rng.ensure(2 * (size_t)n * 8));
-  unsigned long long* rng = ctx->h_rng.as<unsigned long long>();
-  uint64_t out_bound = 0, elig_windows = 0;
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t b = elig[i];
-    rng[2 * i] = bin_off[b];
-    rng[2 * i + 1] = bin_off[b + 1] | (std::min<uint64_t>(bin_win[b], (1u << 24) - 1) << kRangeWinShift);
-    out_bound += std::min<uint64_t>(bin_win[b], max_fill);
-    elig_windows += bin_win[b];
-  }
-  CK(ctx->smem_range.ensure(2 * (size_t)n * 8));
-  CK(ctx->smem_failed.ensure((size_t)n * 4 + 8));
+  CK(ctx->smem_failed.ensure((size_t)n * 16 + 16));
   CK(ctx->out_keys.ensure(std::max<uint64_t>(out_bound, 1) * W * 8));
   CK(ctx->out_counts.ensure(std::max<uint64_t>(out_bound, 1) * 4));
   CK(ctx->counters.ensure(sizeof(Counters)));
-  CK(cudaMemcpyAsync(ctx->smem_range.p, rng, 2 * (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
   Counters* dc = ctx->counters.as<Counters>();
   CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
-  CK(cudaMemsetAsync(&dc->read_work, 0, 8, ctx->stream));  // n_failed
   SmemCountArgs a{};
   a.codes = stream_codes;
   a.desc = desc;
@@ -803,36 +789,37 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   a.out_n = &dc->out_n;
   a.sum_counts = &dc->sum_counts;
   a.distinct = &dc->distinct;
-  a.failed = ctx->smem_failed.as<uint32_t>();
+  a.failed = ctx->smem_failed.as<unsigned long long>();
   a.n_failed = &dc->read_work;
   {
-    Timer tm(ctx, K_COUNT);
+    Timer tm(ctx, K_SMEM);
     CK(launch_count_smem(a, ctx->sms, ctx->stream));
   }
   trace("smem count issued");
   Counters& hc = *ctx->h_counters;
   CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  trace("smem count done (synced)");
   if (hc.out_n > out_bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
   const uint64_t n_failed = hc.read_work;
   Preset pre;
   pre.out_n = hc.out_n;
   pre.sum_counts = hc.sum_counts;
   pre.distinct = hc.distinct;
-  std::vector<uint32_t> failed(n_failed);
-  if (n_failed) {
-    CK(cudaMemcpyAsync(failed.data(), ctx->smem_failed.p, n_failed * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
   uint64_t failed_windows = 0;
-  for (uint32_t li : failed) {
-    rest.push_back(elig[li]);
-    failed_windows += bin_win[elig[li]];
+  if (n_failed) {
+    std::vector<unsigned long long> fr(2 * n_failed);
+    CK(cudaMemcpyAsync(fr.data(), ctx->smem_failed.p, fr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t i = 0; i < n_failed; ++i) {
+      const uint64_t w = fr[2 * i + 1] >> kRangeWinShift;
+      rest.push_back({fr[2 * i], fr[2 * i + 1] & kRangeEndMask, w});
+      failed_windows += w;
+    }
   }
-  trace("smem count done (synced)");
   ctx->stats.smem_bins += n;
   ctx->stats.smem_failed += n_failed;
-  const uint64_t smem_windows = elig_windows - failed_windows;
+  const uint64_t smem_windows = elig_windows - std::min(elig_windows, failed_windows);
   ctx->stats.smem_windows += smem_windows;
   const double smem_obs = smem_windows ? (double)pre.distinct / (double)smem_windows : 0.0;
   gerbil_status st = GERBIL_OK;
@@ -848,39 +835,175 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     ctx->stats.count_sum = pre.sum_counts;
     ctx->stats.owned_windows = total_windows;
   } else {
-    // gather the remaining bins' descriptors into one contiguous range
-    std::sort(rest.begin(), rest.end());
+    // gather the remaining bins' descriptors into one contiguous range (any bin order)
     const uint32_t R = (uint32_t)rest.size();
-    std::vector<unsigned long long> rr(2 * (size_t)R), ro(R);
+    CK(ctx->h_rng.ensure((size_t)R * 16 + (size_t)R * 8));
+    unsigned long long* rr = ctx->h_rng.as<unsigned long long>();
+    unsigned long long* ro = rr + 2 * (size_t)R;
     std::vector<uint64_t> off2(R + 1, 0), win2(R);
     std::vector<uint32_t> list2(R);
     for (uint32_t i = 0; i < R; ++i) {
-      const uint32_t b = rest[i];
-      rr[2 * i] = bin_off[b];
-      rr[2 * i + 1] = bin_off[b + 1];
+      rr[2 * i] = rest[i].d0;
+      rr[2 * i + 1] = rest[i].d1;
       ro[i] = off2[i];
-      off2[i + 1] = off2[i] + (bin_off[b + 1] - bin_off[b]);
-      win2[i] = bin_win[b];
+      off2[i + 1] = off2[i] + (rest[i].d1 - rest[i].d0);
+      win2[i] = rest[i].win;
       list2[i] = i;
     }
-    CK(ctx->rest_range.ensure(rr.size() * 8));
-    CK(ctx->rest_off.ensure(ro.size() * 8));
+    CK(ctx->rest_range.ensure((size_t)R * 16));
+    CK(ctx->rest_off.ensure((size_t)R * 8));
     CK(ctx->rest_desc.ensure(std::max<uint64_t>(off2[R], 1) * 8));
-    CK(cudaMemcpyAsync(ctx->rest_range.p, rr.data(), rr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->rest_off.p, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->rest_range.p, rr, (size_t)R * 16, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->rest_off.p, ro, (size_t)R * 8, cudaMemcpyHostToDevice, ctx->stream));
     {
       Timer tm(ctx, K_SHUFFLE);
       CK(launch_gather_ranges(desc, ctx->rest_range.as<unsigned long long>(), ctx->rest_off.as<unsigned long long>(),
                               R, ctx->rest_desc.as<uint64_t>(), ctx->sms, ctx->stream));
     }
-    const double rho_before = ctx->rho;
     st = count_waves_l2(ctx, stream_codes, ctx->rest_desc.as<uint64_t>(), off2, win2, list2, k, min_count,
                         total_windows, pre);
     if (st != GERBIL_OK) return st;
-    if (ctx->rho == rho_before && smem_obs > 0) ctx->rho = 0.0;  // no wave observation: use the smem one
   }
-  if (smem_obs > 0) ctx->rho = std::min(1.0, std::max(ctx->rho, std::max(smem_obs * 1.15 + 0.01, 0.02)));
+  // ratio adaptation: the larger of the wave and shared-memory observations
+  if (smem_obs > 0) ctx->rho = std::min(1.0, std::max(rest.empty() ? 0.0 : ctx->rho, std::max(smem_obs * 1.15 + 0.01, 0.02)));
   return st;
+}
+
+// Steps (d)+(e) over the bin-ordered descriptors of this rank, bins given on the
+// host: the predicted-small bins go to the shared-memory pass, the rest (and any
+// abandoned bin) to the L2 wave tables (count_waves_ranges); with no small bin the
+// wave tables take the bins in place.
+gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
+                          const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
+                          const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
+                          uint64_t total_windows) {
+  const uint32_t cap = ctx->rec_out ? 0u : smem_slots_for(ctx, k);
+  ctx->stats.smem_slots = cap;
+  if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
+                                      total_windows, Preset{});
+  const uint32_t max_fill = smem_max_fill(cap);
+  const uint64_t thr = smem_window_threshold(ctx, max_fill);
+  std::vector<uint32_t> elig;
+  std::vector<RestBin> rest;
+  for (uint32_t b : bins) {
+    if (bin_off[b + 1] == bin_off[b]) continue;  // no super-mers, nothing to count
+    if (bin_win[b] <= thr) elig.push_back(b);
+    else rest.push_back({bin_off[b], bin_off[b + 1], bin_win[b]});
+  }
+  uint64_t elig_w = 0;
+  for (uint32_t b : elig) elig_w += bin_win[b];
+  // a shared-memory pass over a sliver of the windows would only add a launch and a
+  // gather of every other bin (m < 11 gives few bins small enough): waves take all
+  if (elig.empty() || (ctx->cfg.count_mode != 2 && elig_w * 20 < total_windows))
+    return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count, total_windows,
+                          Preset{});
+  trace("smem bins selected");
+  const uint32_t n = (uint32_t)elig.size();
+  CK(ctx->h_rng.ensure(2 * (size_t)n * 8));
+  unsigned long long* rng = ctx->h_rng.as<unsigned long long>();
+  uint64_t out_bound = 0, elig_windows = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t b = elig[i];
+    rng[2 * i] = bin_off[b];
+    rng[2 * i + 1] = bin_off[b + 1] | (std::min<uint64_t>(bin_win[b], (1u << 24) - 1) << kRangeWinShift);
+    out_bound += std::min<uint64_t>(bin_win[b], max_fill);
+    elig_windows += bin_win[b];
+  }
+  CK(ctx->smem_range.ensure(2 * (size_t)n * 8));
+  CK(cudaMemcpyAsync(ctx->smem_range.p, rng, 2 * (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // h_rng is reused by the wave pass
+  return count_waves_ranges(ctx, stream_codes, desc, n, elig_windows, out_bound, cap, max_fill, rest, k,
+                            min_count, total_windows);
+}
+
+// Single rank with many bins: the per-bin bookkeeping of steps (c)-(e) stays on the
+// device — exclusive scan of the per-bin super-mer counts (bin offsets), scatter, and
+// the split into the shared-memory list and the rest (plan_bins_kernel); only the
+// rest bins (few) come to the host for the wave tables.
+gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
+                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows) {
+  ctx->stats.smem_slots = cap;
+  const unsigned long long* d_win = ctx->hist.as<unsigned long long>();
+  const unsigned long long* d_cnt = d_win + B;
+  CK(ctx->bin_off_d.ensure(((size_t)B + 1) * 8));
+  CK(ctx->p_tmp.ensure(scan_tmp_words(B) * 8));
+  unsigned long long* d_off = ctx->bin_off_d.as<unsigned long long>();
+  CK(launch_scan_u64(reinterpret_cast<const uint64_t*>(d_cnt), reinterpret_cast<uint64_t*>(d_off), B,
+                     ctx->p_tmp.as<uint64_t>(), reinterpret_cast<uint64_t*>(d_off + B), ctx->stream));
+  CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n_sm, 1) * 8));
+  // two-level counting sort: by bin >> kFineShift (shared-memory scatter), then by bin
+  // inside each group (shared-memory cursors, the group's output range stays in L2)
+  constexpr uint32_t kFineShift = 10;
+  const uint32_t groups = ((B - 1) >> kFineShift) + 1;
+  CK(ctx->cursor.ensure((size_t)groups * 8));
+  CK(cudaMemcpy2DAsync(ctx->cursor.p, 8, d_off, (size_t)8 << kFineShift, 8, groups, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));  // level-1 output (reuses exchange buffers)
+  CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
+  ScatterArgs s{};
+  s.desc_in = ctx->desc_pre.as<uint64_t>();
+  s.bin_in = ctx->bin_pre.as<uint32_t>();
+  s.n = n_sm;
+  s.n_bins = B;
+  s.bin_shift = kFineShift;
+  s.cursor = ctx->cursor.as<unsigned long long>();
+  s.desc_out = ctx->send_desc.as<uint64_t>();
+  s.bin_out = ctx->send_bin.as<uint32_t>();
+  {
+    Timer tm(ctx, K_SHUFFLE, nullptr, true, 2);
+    CK(launch_scatter(s, ctx->sms, ctx->stream));
+    CK(launch_regroup_fine(ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), d_off, B, kFineShift,
+                           ctx->desc_sorted.as<uint64_t>(), ctx->stream));
+  }
+  trace("scatter issued");
+  const uint32_t max_fill = smem_max_fill(cap);
+  CK(ctx->smem_range.ensure((size_t)B * 16));
+  CK(ctx->rest_range.ensure((size_t)B * 24));
+  CK(ctx->plan_sums.ensure(5 * 8));
+  CK(cudaMemsetAsync(ctx->plan_sums.p, 0, 5 * 8, ctx->stream));
+  PlanBinsArgs pa{};
+  pa.win = d_win;
+  pa.off = d_off;
+  pa.n_bins = B;
+  pa.thr = smem_window_threshold(ctx, max_fill);
+  pa.max_fill = max_fill;
+  pa.elig = ctx->smem_range.as<unsigned long long>();
+  pa.rest = ctx->rest_range.as<unsigned long long>();
+  pa.sums = ctx->plan_sums.as<unsigned long long>();
+  pa.max_win = pa.sums + 4;
+  {
+    Timer tm(ctx, K_SHUFFLE);
+    CK(launch_plan_bins(pa, ctx->sms, ctx->stream));
+  }
+  unsigned long long sums[5];
+  CK(cudaMemcpyAsync(sums, pa.sums, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const uint64_t n_elig = sums[0], n_rest = sums[3];
+  ctx->stats.max_bin_windows = sums[4];
+  std::vector<RestBin> rest(n_rest);
+  if (n_rest) {
+    static_assert(sizeof(RestBin) == 24, "RestBin mirrors the device rest triples");
+    CK(cudaMemcpyAsync(rest.data(), pa.rest, n_rest * 24, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  trace("bins planned on the device");
+  if (n_elig == 0) {
+    // nothing for shared memory: the wave tables take every bin
+    std::vector<uint64_t> off2(n_rest + 1, 0), win2(n_rest);
+    std::vector<uint32_t> list2(n_rest);
+    std::sort(rest.begin(), rest.end(), [](const RestBin& x, const RestBin& y) { return x.d0 < y.d0; });
+    // bins are consecutive in desc_sorted (all of them are rest bins): no gather needed
+    for (uint64_t i = 0; i < n_rest; ++i) {
+      off2[i] = rest[i].d0;
+      off2[i + 1] = rest[i].d1;
+      win2[i] = rest[i].win;
+      list2[i] = (uint32_t)i;
+    }
+    return count_waves_l2(ctx, codes, ctx->desc_sorted.as<uint64_t>(), off2, win2, list2, k, min_count, windows,
+                          Preset{});
+  }
+  return count_waves_ranges(ctx, codes, ctx->desc_sorted.as<uint64_t>(), (uint32_t)n_elig, sums[1], sums[2], cap,
+                            max_fill, rest, k, min_count, windows);
 }
 
 // ---------------------------------------------------------------------------
@@ -1066,6 +1189,13 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   const uint64_t local_windows = ctx->h_counters->n_windows;
   ctx->stats.supermers = n_sm;
   ctx->stats.valid_windows = local_windows;
+  uint64_t owned_windows = 0;
+  const uint32_t smem_cap = (!ctx->comm && !ctx->rec_out && B >= kDevicePlanBins) ? smem_slots_for(ctx, k) : 0u;
+  if (smem_cap) {
+    // many bins, one rank: steps (c)-(e) planned on the device (no per-bin host work)
+    CKS(count_local_device_plan(ctx, codes, n_sm, B, smem_cap, k, min_count, local_windows));
+    owned_windows = local_windows;
+  } else {
   CK(ctx->h_hist.ensure(3ull * B * 8));
   const unsigned long long* hist = ctx->h_hist.as<unsigned long long>();
   CK(cudaMemcpyAsync(ctx->h_hist.p, ctx->hist.p, 3ull * B * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1076,7 +1206,6 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   std::vector<uint32_t> owned;
   owned.reserve(B);
   const uint64_t* stream_codes = codes;
-  uint64_t owned_windows = 0;
   if (!ctx->comm) {
     // (c) local: group descriptors by bin
     for (uint32_t b = 0; b < B; ++b) {
@@ -1217,6 +1346,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   trace("scatter issued");
   CKS(count_waves(ctx, stream_codes, ctx->desc_sorted.as<uint64_t>(), bin_off, bin_win, owned, k,
                   min_count, owned_windows));
+  }
   // Σ-count invariant: every valid window counted exactly once
   if (ctx->stats.count_sum != owned_windows)
     return fail(ctx, GERBIL_E_INTERNAL,
@@ -1233,15 +1363,17 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
     ctx->stats.ms_h2d = ms[K_H2D];
     ctx->stats.ms_supermer = ms[K_SUPERMER];
     ctx->stats.ms_shuffle = ms[K_SHUFFLE];
-    ctx->stats.ms_count = ms[K_COUNT];
+    ctx->stats.ms_count = ms[K_COUNT] + ms[K_SMEM];
+    ctx->stats.ms_smem = ms[K_SMEM];
     ctx->stats.ms_compact = ms[K_COMPACT];
     ctx->stats.ms_overflow = ms[K_OVERFLOW];
   }
   // kernel launches of this call (copies are not launches)
-  ctx->stats.launches_count = ctx->n_launch[K_COUNT];
+  ctx->stats.launches_count = ctx->n_launch[K_COUNT] + ctx->n_launch[K_SMEM];
+  ctx->stats.launches_smem = ctx->n_launch[K_SMEM];
   ctx->stats.launches_compact = ctx->n_launch[K_COMPACT];
   ctx->stats.launches_total = ctx->n_launch[K_SUPERMER] + ctx->n_launch[K_SHUFFLE] + ctx->n_launch[K_COUNT] +
-                              ctx->n_launch[K_COMPACT] + ctx->n_launch[K_OVERFLOW];
+                              ctx->n_launch[K_COMPACT] + ctx->n_launch[K_OVERFLOW] + ctx->n_launch[K_SMEM];
   ctx->stats.ms_total = wall_ms() - t0;
   ctx->have_result = true;
   return GERBIL_OK;
@@ -1279,7 +1411,7 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
   if (!(cfg.dfp_pivot >= 0.0 && cfg.dfp_pivot <= 1.0)) return GERBIL_E_USAGE;
   if (cfg.order_sample_stride == 0) cfg.order_sample_stride = 16;
   if (cfg.world > 1 && !cfg.nccl_unique_id) return GERBIL_E_USAGE;
-  if (cfg.n_bins > (1u << 20)) return GERBIL_E_USAGE;
+  if (cfg.n_bins > (1u << 22)) return GERBIL_E_USAGE;
   if (cfg.max_probes == 0) cfg.max_probes = 32;
   if (cfg.target_load <= 0) cfg.target_load = 0.7;
   if (cfg.target_load > 4.0) return GERBIL_E_USAGE;

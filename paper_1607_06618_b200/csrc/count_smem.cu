@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
         for (uint32_t s = lane; s < cb; s += 32) T.clear(s);
         if (lane == 0) {
           const unsigned long long e = atomicAdd(a.n_failed, 1ull);
-          a.failed[e] = l0;
+          a.failed[2 * e] = a.range[2 * (size_t)l0];  // the bin's range entry, for the L2 recount
+          a.failed[2 * e + 1] = a.range[2 * (size_t)l0 + 1];
         }
       }
       __syncwarp();
@@ -476,7 +477,7 @@ __global__ void gather_ranges_kernel(const uint64_t* __restrict__ src, const uns
 
 template <int W, bool PACK>
 cudaError_t launch_smem(const SmemCountArgs& a, int sms, cudaStream_t st) {
-  const int warps = smem_count_warps();
+  const int warps = smem_count_warps(a.k);
   const uint32_t wb = smem_warp_bytes(a.k, a.cap);
   SmemCountArgs b = a;
   if (const char* e = getenv("GERBIL_SMEM_DBG")) b.dbg = (uint32_t)atoi(e);
@@ -494,13 +495,16 @@ cudaError_t launch_smem(const SmemCountArgs& a, int sms, cudaStream_t st) {
 
 }  // namespace
 
-int smem_count_warps() {
-  static int w = [] {
+// Warps per CTA (one CTA per SM): more warps hide more latency (the insert chain is a
+// string of dependent shared-memory round trips) but split the shared memory into
+// smaller tables. 16 for the 17-byte slots of k <= 48, 8 up to W = 3, else 4.
+int smem_count_warps(uint32_t k) {
+  static const int env = [] {
     const char* e = getenv("GERBIL_SMEM_WARPS");
-    int v = (e && *e) ? atoi(e) : 8;
-    return v < 1 ? 1 : (v > kSmemMaxWarps ? kSmemMaxWarps : v);
+    return (e && *e) ? atoi(e) : 0;
   }();
-  return w;
+  int v = env ? env : (smem_pack(k) ? 16 : (key_words(k) <= 3 ? 8 : 4));
+  return v < 1 ? 1 : (v > kSmemMaxWarps ? kSmemMaxWarps : v);
 }
 
 uint32_t smem_slot_bytes(uint32_t k) { return (smem_pack(k) ? 16u : 8u * key_words(k) + 4u) + 1u /* tag */; }
@@ -510,7 +514,7 @@ uint32_t smem_warp_bytes(uint32_t k, uint32_t cap) {
 }
 
 uint32_t smem_table_slots(uint32_t k, size_t smem_per_block) {
-  const int warps = smem_count_warps();
+  const int warps = smem_count_warps(k);
   const size_t per_warp = smem_per_block / warps;
   const uint32_t ovh = smem_overhead(smem_stage_words(smem_pack(k)));
   if (per_warp <= ovh + 64u * 16u) return 0;
@@ -527,6 +531,65 @@ cudaError_t launch_gather_ranges(const uint64_t* src, const unsigned long long* 
   uint64_t grid = (n + 7) / 8;
   if (grid > (uint64_t)sms * 8) grid = (uint64_t)sms * 8;
   gather_ranges_kernel<<<(unsigned)grid, 256, 0, st>>>(src, ranges, dst_off, n, dst);
+  return cudaGetLastError();
+}
+
+// Device-side bin plan (single rank, many bins): per bin with super-mers, either an
+// entry of the shared-memory list (predicted to fit: windows <= thr) or a rest triple
+// (first descriptor, end descriptor, windows) for the L2 wave tables.
+__global__ void plan_bins_kernel(PlanBinsArgs a) {
+  // warp-aggregated: one atomic per warp and counter (4M bins would serialise on them)
+  const uint32_t lane = lane_id();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < a.n_bins; base += stride) {
+    const uint32_t b = base + threadIdx.x;
+    unsigned long long w = 0, d0 = 0, d1 = 0;
+    bool has = false;
+    if (b < a.n_bins) {
+      w = a.win[b];
+      d0 = a.off[b];
+      d1 = a.off[b + 1];
+      has = d1 != d0;
+    }
+    const bool el = has && w <= a.thr, rs = has && !el;
+    const uint32_t me = __ballot_sync(kFull, el), mr = __ballot_sync(kFull, rs);
+    unsigned long long we = el ? w : 0ull, wf = el ? (w < a.max_fill ? w : (unsigned long long)a.max_fill) : 0ull,
+                       wm = has ? w : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      we += __shfl_xor_sync(kFull, we, o);
+      wf += __shfl_xor_sync(kFull, wf, o);
+      wm = max(wm, __shfl_xor_sync(kFull, wm, o));
+    }
+    unsigned long long be = 0, br = 0;
+    if (lane == 0) {
+      if (me) be = atomicAdd(&a.sums[0], (unsigned long long)__popc(me));
+      if (mr) br = atomicAdd(&a.sums[3], (unsigned long long)__popc(mr));
+      if (we) atomicAdd(&a.sums[1], we);
+      if (wf) atomicAdd(&a.sums[2], wf);
+      if (wm) atomicMax(a.max_win, wm);
+    }
+    be = __shfl_sync(kFull, be, 0);
+    br = __shfl_sync(kFull, br, 0);
+    const uint32_t below = (1u << lane) - 1u;
+    if (el) {
+      const unsigned long long i = be + __popc(me & below);
+      a.elig[2 * i] = d0;
+      a.elig[2 * i + 1] = d1 | ((w < (1ull << 24) ? w : (1ull << 24) - 1) << kRangeWinShift);
+    } else if (rs) {
+      const unsigned long long i = br + __popc(mr & below);
+      a.rest[3 * i] = d0;
+      a.rest[3 * i + 1] = d1;
+      a.rest[3 * i + 2] = w;
+    }
+  }
+}
+
+cudaError_t launch_plan_bins(const PlanBinsArgs& a, int sms, cudaStream_t st) {
+  if (a.n_bins == 0) return cudaSuccess;
+  uint64_t grid = (a.n_bins + 255) / 256;
+  if (grid > (uint64_t)sms * 8) grid = (uint64_t)sms * 8;
+  plan_bins_kernel<<<(unsigned)grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

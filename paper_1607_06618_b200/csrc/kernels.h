@@ -88,8 +88,14 @@ struct ScatterArgs {
   uint32_t* bin_out;           // optional (nullptr)
   uint64_t pos_add;            // added to pos (rebasing received super-mers)
   const unsigned char* keep;   // optional per-bin filter (owned bins) or nullptr
+  uint32_t bin_shift;          // group by bin_in >> bin_shift (bin_out keeps the full bin); 0 = by bin
 };
 cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t s);
+// Second level of a two-level scatter: descriptors already grouped by bin >> shift
+// (group g = [off[g << shift], off[min((g + 1) << shift, n_bins)]) of desc_in/bin_in)
+// are regrouped by bin inside each group with shared-memory cursors.
+cudaError_t launch_regroup_fine(const uint64_t* desc_in, const uint32_t* bin_in, const unsigned long long* off,
+                                uint32_t n_bins, uint32_t shift, uint64_t* desc_out, cudaStream_t s);
 
 // world > 1: copy every local super-mer (descriptor + word-aligned payload)
 // into the send buffer, ordered by (destination rank, bin).
@@ -149,15 +155,27 @@ struct SmemCountArgs {
   unsigned long long* out_n;
   unsigned long long* sum_counts;
   unsigned long long* distinct;
-  uint32_t* failed;                  // [n_list] list indices of abandoned bins
+  unsigned long long* failed;        // [n_list][2] range entries of abandoned bins
   unsigned long long* n_failed;
   uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 4 = no tag fast path
 };
-int smem_count_warps();                                      // warps per CTA (GERBIL_SMEM_WARPS, default 8)
+int smem_count_warps(uint32_t k);                            // warps per CTA (GERBIL_SMEM_WARPS overrides)
 uint32_t smem_slot_bytes(uint32_t k);
 uint32_t smem_warp_bytes(uint32_t k, uint32_t cap);
 uint32_t smem_table_slots(uint32_t k, size_t smem_per_block);  // 0 = no room
 cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);
+struct PlanBinsArgs {
+  const unsigned long long* win;   // [n_bins] windows per bin (step b histogram)
+  const unsigned long long* off;   // [n_bins + 1] first descriptor of each bin (exclusive scan)
+  uint32_t n_bins;
+  unsigned long long thr;          // shared-memory list iff windows <= thr
+  uint32_t max_fill;
+  unsigned long long* elig;        // [n_bins][2] shared-memory list (range entries, kRangeWinShift)
+  unsigned long long* rest;        // [n_bins][3] first descriptor, end descriptor, windows
+  unsigned long long* sums;        // [4]: n_elig, Σ elig windows, Σ min(windows, max_fill), n_rest (zeroed)
+  unsigned long long* max_win;     // (zeroed)
+};
+cudaError_t launch_plan_bins(const PlanBinsArgs& a, int sms, cudaStream_t s);
 // dst[dst_off[i] + j] = src[ranges[2i] + j] for j < ranges[2i+1] - ranges[2i]
 cudaError_t launch_gather_ranges(const uint64_t* src, const unsigned long long* ranges,
                                  const unsigned long long* dst_off, uint32_t n, uint64_t* dst, int sms,

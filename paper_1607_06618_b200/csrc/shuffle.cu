@@ -25,9 +25,10 @@ __global__ void __launch_bounds__(kThreads)
 scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
   extern __shared__ uint32_t s_mem[];
   uint32_t* s_cnt = s_mem;                                   // [n_bins]
-  unsigned long long* s_base = (unsigned long long*)(s_mem + ((a.n_bins + 1) & ~1u));
+  const uint32_t nb = ((a.n_bins - 1) >> a.bin_shift) + 1;  // groups (bins when bin_shift == 0)
+  unsigned long long* s_base = (unsigned long long*)(s_mem + ((nb + 1) & ~1u));
   const uint32_t tid = threadIdx.x;
-  for (uint32_t b = tid; b < a.n_bins; b += kThreads) s_cnt[b] = 0;
+  for (uint32_t b = tid; b < nb; b += kThreads) s_cnt[b] = 0;
   __syncthreads();
   for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
     const uint64_t i0 = c * kChunk;
@@ -38,7 +39,7 @@ scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
       const uint64_t i = i0 + j * kThreads + tid;
       bins[j] = 0xffffffffu;
       if (i < a.n) {
-        const uint32_t b = a.bin_in[i];
+        const uint32_t b = a.bin_in[i] >> a.bin_shift;
         if (!a.keep || a.keep[b]) {
           bins[j] = b;
           desc[j] = a.desc_in[i];
@@ -57,7 +58,7 @@ scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
       if (bins[j] != 0xffffffffu) {
         const uint64_t d = s_base[bins[j]] + rank[j];
         a.desc_out[d] = desc[j] + (a.pos_add << kNwinBits);
-        if (a.bin_out) a.bin_out[d] = bins[j];
+        if (a.bin_out) a.bin_out[d] = a.bin_shift ? a.bin_in[i0 + j * kThreads + tid] : bins[j];
       }
     __syncthreads();
 #pragma unroll
@@ -70,11 +71,11 @@ scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
 __global__ void scatter_global_kernel(ScatterArgs a) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = a.bin_in[i];
+    const uint32_t b = a.bin_in[i] >> a.bin_shift;
     if (a.keep && !a.keep[b]) continue;
     const uint64_t d = atomicAdd(&a.cursor[b], 1ull);
     a.desc_out[d] = a.desc_in[i] + (a.pos_add << kNwinBits);
-    if (a.bin_out) a.bin_out[d] = b;
+    if (a.bin_out) a.bin_out[d] = a.bin_in[i];
   }
 }
 
@@ -106,7 +107,36 @@ __global__ void pack_kernel(PackArgs a) {
   }
 }
 
+constexpr int kFineThreads = 512;
+
+__global__ void __launch_bounds__(kFineThreads) regroup_fine_kernel(const uint64_t* __restrict__ desc_in,
+                                                                    const uint32_t* __restrict__ bin_in,
+                                                                    const unsigned long long* __restrict__ off,
+                                                                    uint32_t n_bins, uint32_t shift,
+                                                                    uint64_t* __restrict__ desc_out) {
+  extern __shared__ uint32_t s_cur[];  // [1 << shift] cursors relative to the group's first descriptor
+  const uint32_t g = blockIdx.x, fan = 1u << shift, b0 = g << shift;
+  const uint32_t b1 = min(b0 + fan, n_bins);
+  const uint64_t i0 = off[b0], i1 = off[b1];
+  for (uint32_t t = threadIdx.x; t < fan; t += blockDim.x) s_cur[t] = b0 + t < b1 ? (uint32_t)(off[b0 + t] - i0) : 0u;
+  __syncthreads();
+  for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t b = bin_in[i] & (fan - 1u);
+    const uint32_t p = atomicAdd(&s_cur[b], 1u);
+    desc_out[i0 + p] = desc_in[i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_regroup_fine(const uint64_t* desc_in, const uint32_t* bin_in, const unsigned long long* off,
+                                uint32_t n_bins, uint32_t shift, uint64_t* desc_out, cudaStream_t st) {
+  const uint32_t groups = (n_bins + (1u << shift) - 1) >> shift;
+  if (groups == 0) return cudaSuccess;
+  regroup_fine_kernel<<<groups, kFineThreads, (size_t)4 << shift, st>>>(desc_in, bin_in, off, n_bins, shift,
+                                                                         desc_out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack(const PackArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
@@ -116,8 +146,9 @@ cudaError_t launch_pack(const PackArgs& a, int sms, cudaStream_t st) {
 
 cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
-  if (a.n_bins <= 16384) {
-    const size_t dyn = (size_t)((a.n_bins + 1) & ~1u) * 4 + (size_t)a.n_bins * 8;
+  const uint32_t nb = ((a.n_bins - 1) >> a.bin_shift) + 1;  // groups the kernel sees
+  if (nb <= 16384) {
+    const size_t dyn = (size_t)((nb + 1) & ~1u) * 4 + (size_t)nb * 8;
     cudaError_t e = cudaFuncSetAttribute(scatter_smem_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;

@@ -104,6 +104,8 @@ class Stats(C.Structure):
         ("smem_failed", C.c_uint64),
         ("smem_windows", C.c_uint64),
         ("smem_slots", C.c_uint32),
+        ("launches_smem", C.c_uint32),
+        ("ms_smem", C.c_double),
     ]
 
     def as_dict(self) -> dict:
