@@ -819,7 +819,77 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   }
   ctx->stats.smem_bins += n;
   ctx->stats.smem_failed += n_failed;
-  const uint64_t smem_windows = elig_windows - std::min(elig_windows, failed_windows);
+  uint64_t smem_windows = elig_windows - std::min(elig_windows, failed_windows);
+  // Tier 2: bins too large for the many-warp tables get 4-warp tables (~4x the slots per
+  // warp) in a second launch; what still does not fit goes to the wave tables.
+  const int w1 = a.warps ? a.warps : smem_count_warps(k);
+  const int w2n = std::max(1, w1 / 2);
+  const uint32_t cap2 = w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u;
+  if (!rest.empty() && cap2 > cap) {
+    const uint32_t mf2 = smem_max_fill(cap2);
+    const uint64_t thr2 = smem_window_threshold(ctx, mf2);
+    std::vector<RestBin> keep;
+    uint64_t n2 = 0, w2 = 0, ob2 = 0;
+    CK(ctx->h_rng.ensure(rest.size() * 16));
+    unsigned long long* r2 = ctx->h_rng.as<unsigned long long>();
+    for (const RestBin& rb : rest) {
+      if (rb.win <= thr2) {
+        r2[2 * n2] = rb.d0;
+        r2[2 * n2 + 1] = rb.d1 | (std::min<uint64_t>(rb.win, (1u << 24) - 1) << kRangeWinShift);
+        ++n2;
+        w2 += rb.win;
+        ob2 += std::min<uint64_t>(rb.win, mf2);
+      } else {
+        keep.push_back(rb);
+      }
+    }
+    if (n2) {
+      const uint64_t out2 = pre.out_n + ob2;
+      CK(ensure_keep(ctx->out_keys, out2 * W * 8, pre.out_n * W * 8, ctx->stream));
+      CK(ensure_keep(ctx->out_counts, out2 * 4, pre.out_n * 4, ctx->stream));
+      CK(ctx->smem_range.ensure(n2 * 16));
+      CK(ctx->smem_failed.ensure(n2 * 16 + 16));
+      CK(cudaMemcpyAsync(ctx->smem_range.p, r2, n2 * 16, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemsetAsync(&dc->read_work, 0, 8, ctx->stream));
+      SmemCountArgs a2 = a;
+      a2.range = ctx->smem_range.as<unsigned long long>();
+      a2.n_list = (uint32_t)n2;
+      a2.cap = cap2;
+      a2.max_fill = mf2;
+      a2.warps = w2n;
+      a2.out_keys = ctx->out_keys.as<uint64_t>();
+      a2.out_counts = ctx->out_counts.as<uint32_t>();
+      a2.out_cap = out2;
+      a2.failed = ctx->smem_failed.as<unsigned long long>();
+      {
+        Timer tm(ctx, K_SMEM);
+        CK(launch_count_smem(a2, ctx->sms, ctx->stream));
+      }
+      CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (hc.out_n > out2) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+      pre.out_n = hc.out_n;
+      pre.sum_counts = hc.sum_counts;
+      pre.distinct = hc.distinct;
+      const uint64_t nf2 = hc.read_work;
+      uint64_t fw2 = 0;
+      if (nf2) {
+        std::vector<unsigned long long> fr(2 * nf2);
+        CK(cudaMemcpyAsync(fr.data(), ctx->smem_failed.p, fr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (uint64_t i = 0; i < nf2; ++i) {
+          const uint64_t w = fr[2 * i + 1] >> kRangeWinShift;
+          keep.push_back({fr[2 * i], fr[2 * i + 1] & kRangeEndMask, w});
+          fw2 += w;
+        }
+      }
+      ctx->stats.smem_bins += n2;
+      ctx->stats.smem_failed += nf2;
+      smem_windows += w2 - std::min(w2, fw2);
+      rest.swap(keep);
+      trace("smem tier 2 done (synced)");
+    }
+  }
   ctx->stats.smem_windows += smem_windows;
   const double smem_obs = smem_windows ? (double)pre.distinct / (double)smem_windows : 0.0;
   gerbil_status st = GERBIL_OK;

@@ -477,7 +477,7 @@ __global__ void gather_ranges_kernel(const uint64_t* __restrict__ src, const uns
 
 template <int W, bool PACK>
 cudaError_t launch_smem(const SmemCountArgs& a, int sms, cudaStream_t st) {
-  const int warps = smem_count_warps(a.k);
+  const int warps = a.warps ? a.warps : smem_count_warps(a.k);
   const uint32_t wb = smem_warp_bytes(a.k, a.cap);
   SmemCountArgs b = a;
   if (const char* e = getenv("GERBIL_SMEM_DBG")) b.dbg = (uint32_t)atoi(e);
@@ -513,8 +513,8 @@ uint32_t smem_warp_bytes(uint32_t k, uint32_t cap) {
   return (smem_overhead(smem_stage_words(smem_pack(k))) + cap * smem_slot_bytes(k) + 15u) & ~15u;
 }
 
-uint32_t smem_table_slots(uint32_t k, size_t smem_per_block) {
-  const int warps = smem_count_warps(k);
+uint32_t smem_table_slots(uint32_t k, size_t smem_per_block, int warps_in) {
+  const int warps = warps_in ? warps_in : smem_count_warps(k);
   const size_t per_warp = smem_per_block / warps;
   const uint32_t ovh = smem_overhead(smem_stage_words(smem_pack(k)));
   if (per_warp <= ovh + 64u * 16u) return 0;

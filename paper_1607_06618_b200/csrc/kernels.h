@@ -158,11 +158,12 @@ struct SmemCountArgs {
   unsigned long long* failed;        // [n_list][2] range entries of abandoned bins
   unsigned long long* n_failed;
   uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 4 = no tag fast path
+  int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match
 };
 int smem_count_warps(uint32_t k);                            // warps per CTA (GERBIL_SMEM_WARPS overrides)
 uint32_t smem_slot_bytes(uint32_t k);
 uint32_t smem_warp_bytes(uint32_t k, uint32_t cap);
-uint32_t smem_table_slots(uint32_t k, size_t smem_per_block);  // 0 = no room
+uint32_t smem_table_slots(uint32_t k, size_t smem_per_block, int warps = 0);  // 0 = no room
 cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);
 struct PlanBinsArgs {
   const unsigned long long* win;   // [n_bins] windows per bin (step b histogram)
