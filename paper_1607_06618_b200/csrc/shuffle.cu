@@ -17,12 +17,12 @@
 namespace gerbil {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kPer = 8;
-constexpr int kChunk = kThreads * kPer;
-
+// kThreads x kPer descriptors per CTA chunk: one global atomic per (chunk, distinct bin),
+// so many bins want big chunks (2048 for <= 2048 bins, 8192 above).
+template <int kThreads, int kPer>
 __global__ void __launch_bounds__(kThreads)
 scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
+  constexpr int kChunk = kThreads * kPer;
   extern __shared__ uint32_t s_mem[];
   uint32_t* s_cnt = s_mem;                                   // [n_bins]
   const uint32_t nb = ((a.n_bins - 1) >> a.bin_shift) + 1;  // groups (bins when bin_shift == 0)
@@ -149,16 +149,21 @@ cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t st) {
   const uint32_t nb = ((a.n_bins - 1) >> a.bin_shift) + 1;  // groups the kernel sees
   if (nb <= 16384) {
     const size_t dyn = (size_t)((nb + 1) & ~1u) * 4 + (size_t)nb * 8;
-    cudaError_t e = cudaFuncSetAttribute(scatter_smem_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    auto run = [&](auto kern, int threads, int per) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return e;
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, dyn);
+      if (per_sm < 1) per_sm = 1;
+      const uint64_t chunk = (uint64_t)threads * per;
+      const uint64_t n_chunks = (a.n + chunk - 1) / chunk;
+      uint64_t grid = (uint64_t)sms * per_sm;
+      if (grid > n_chunks) grid = n_chunks;
+      kern<<<(unsigned)grid, threads, dyn, st>>>(a, n_chunks);
+      return cudaSuccess;
+    };
+    cudaError_t e = nb <= 2048 ? run(scatter_smem_kernel<256, 8>, 256, 8) : run(scatter_smem_kernel<512, 16>, 512, 16);
     if (e != cudaSuccess) return e;
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scatter_smem_kernel, kThreads, dyn);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t n_chunks = (a.n + kChunk - 1) / kChunk;
-    uint64_t grid = (uint64_t)sms * per_sm;
-    if (grid > n_chunks) grid = n_chunks;
-    scatter_smem_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(a, n_chunks);
   } else {
     scatter_global_kernel<<<sms * 8, 256, 0, st>>>(a);
   }
