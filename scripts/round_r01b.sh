@@ -14,14 +14,14 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 ARGS="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py $ARGS > gpurun_out/ncu_launches.log 2>&1; echo "launches rc=$?" >> gpurun_out/summary.txt
-cap() {  # name regex skip
-  timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:$2 -s $3 -c 1 \
+cap() {  # name regex skip [count]
+  timeout 900 ncu --set full --clock-control none --cache-control none --import-source on -k regex:$2 -s $3 -c ${4:-1} \
      -o gpurun_out/prof_$1 python bench.py $ARGS > gpurun_out/ncu_$1.log 2>&1
   echo "$1 rc=$?" >> gpurun_out/summary.txt
 }
-cap smem count_smem 3
+# 3 warm-up steps x 2 shared-memory launches (tiers 1 and 2): the timed step's pair
+cap smem count_smem 6 2
 cap supermer supermer_kernel 3
 cap regroup regroup_fine 3
 cap scatter scatter_smem 3
-cap waves count_inline 30
 cat gpurun_out/summary.txt
