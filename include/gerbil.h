@@ -113,7 +113,8 @@ typedef struct {
                               0 = auto: a bin predicted (ρ̂ · windows) to fit one warp's
                                   shared-memory table is counted there, the rest in
                                   L2-resident wave tables; n_bins = 0 then picks enough bins
-                                  (up to 2^20) when m >= 11 makes bins that small;
+                                  (up to 2^22) when m >= 11 makes bins that small and
+                                  k <= 96 (where it was measured to win);
                               1 = L2 wave tables only;
                               2 = try shared memory for every bin (test seam: bins that
                                   overflow it are recounted in the wave tables).

@@ -336,7 +336,10 @@ uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, 
   // fit one warp's table: ~0.35 of its slots on average leaves room for
   // skew. Bins are hashes of minimizers, so that needs many more minimizers
   // than bins (m >= 11: >= 2M canonical m-mers) — else the L2 policy below.
-  const uint32_t cap = (ctx->rec_out || m < 11) ? 0u : smem_slots_for(ctx, k);
+  // Measured at C1 scale: the shared-memory path wins for k <= 96 (W <= 3:
+  // 1.1x at k = 40, 1.7x at k = 56, 1.5x at k = 65) and loses for k = 100 (one window per
+  // 100-bp read) and k = 200 (tables too small for its bins) — those keep the L2 policy.
+  const uint32_t cap = (ctx->rec_out || m < 11 || key_words(k) > 3) ? 0u : smem_slots_for(ctx, k);
   if (cap) {
     const double want = ctx->rho * (double)n_bases * ctx->world / (0.35 * cap);
     uint32_t B = 512;
