@@ -162,7 +162,7 @@ cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t st) {
       kern<<<(unsigned)grid, threads, dyn, st>>>(a, n_chunks);
       return cudaSuccess;
     };
-    cudaError_t e = nb <= 2048 ? run(scatter_smem_kernel<256, 8>, 256, 8) : run(scatter_smem_kernel<512, 16>, 512, 16);
+    cudaError_t e = nb <= 2048 ? run(scatter_smem_kernel<256, 8>, 256, 8) : run(scatter_smem_kernel<1024, 8>, 1024, 8);
     if (e != cudaSuccess) return e;
   } else {
     scatter_global_kernel<<<sms * 8, 256, 0, st>>>(a);
