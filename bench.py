@@ -214,7 +214,9 @@ def main() -> None:
         obj = [gerbil.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    n_bins = args.bins or ((1 << 20 if M >= 11 else 4096) if world > 1 else 0)
+    # N > 1: ranks need the same explicit B; the multi-rank plan (LPT over all bins) runs on the
+    # host, so keep B moderate there (L2 wave tables); N = 1 lets the library pick (4M bins, m = 15)
+    n_bins = args.bins or (4096 if world > 1 else 0)
     g = gerbil.Gerbil(device=local, rank=rank, world=world, unique_id=uid, n_bins=n_bins,
                       stream=stream.cuda_stream, timing=True,
                       wave_table_bytes=args.table_mb << 20, count_mode=args.count_mode)
