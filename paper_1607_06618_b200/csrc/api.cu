@@ -328,7 +328,8 @@ uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k);
 // from this many bins up, a single rank plans steps (c)-(e) on the device
 constexpr uint32_t kDevicePlanBins = 1u << 16;
 gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
-                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows);
+                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows,
+                                      uint64_t n_bases);
 
 uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, uint32_t m) {
   if (ctx->cfg.n_bins) return ctx->cfg.n_bins;
@@ -994,7 +995,8 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
 // the split into the shared-memory list and the rest (plan_bins_kernel); only the
 // rest bins (few) come to the host for the wave tables.
 gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
-                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows) {
+                                      uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows,
+                                      uint64_t n_bases) {
   ctx->stats.smem_slots = cap;
   const unsigned long long* d_win = ctx->hist.as<unsigned long long>();
   const unsigned long long* d_cnt = d_win + B;
@@ -1021,12 +1023,20 @@ gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, ui
   s.bin_shift = kFineShift;
   s.cursor = ctx->cursor.as<unsigned long long>();
   s.desc_out = ctx->send_desc.as<uint64_t>();
-  s.bin_out = ctx->send_bin.as<uint32_t>();
+  // descriptors below 2^54 (positions < 2^43 bases) carry the fine bin in their top bits:
+  // the first level then stores 8 bytes per super-mer instead of 8 + 4 at two addresses
+  const bool pack = n_bases < (1ull << 43);
+  if (pack) s.pack_low_bits = kFineShift;
+  else s.bin_out = ctx->send_bin.as<uint32_t>();
   {
     Timer tm(ctx, K_SHUFFLE, nullptr, true, 2);
     CK(launch_scatter(s, ctx->sms, ctx->stream));
-    CK(launch_regroup_fine(ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), d_off, B, kFineShift,
-                           ctx->desc_sorted.as<uint64_t>(), ctx->stream));
+    if (pack)
+      CK(launch_regroup_fine_packed(ctx->send_desc.as<uint64_t>(), d_off, B, kFineShift,
+                                    ctx->desc_sorted.as<uint64_t>(), ctx->stream));
+    else
+      CK(launch_regroup_fine(ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), d_off, B, kFineShift,
+                             ctx->desc_sorted.as<uint64_t>(), ctx->stream));
   }
   trace("scatter issued");
   const uint32_t max_fill = smem_max_fill(cap);
@@ -1266,7 +1276,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   const uint32_t smem_cap = (!ctx->comm && !ctx->rec_out && B >= kDevicePlanBins) ? smem_slots_for(ctx, k) : 0u;
   if (smem_cap) {
     // many bins, one rank: steps (c)-(e) planned on the device (no per-bin host work)
-    CKS(count_local_device_plan(ctx, codes, n_sm, B, smem_cap, k, min_count, local_windows));
+    CKS(count_local_device_plan(ctx, codes, n_sm, B, smem_cap, k, min_count, local_windows, n_bases));
     owned_windows = local_windows;
   } else {
   CK(ctx->h_hist.ensure(3ull * B * 8));

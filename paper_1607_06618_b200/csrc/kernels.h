@@ -89,13 +89,19 @@ struct ScatterArgs {
   uint64_t pos_add;            // added to pos (rebasing received super-mers)
   const unsigned char* keep;   // optional per-bin filter (owned bins) or nullptr
   uint32_t bin_shift;          // group by bin_in >> bin_shift (bin_out keeps the full bin); 0 = by bin
+  uint32_t pack_low_bits;      // > 0: no bin_out; the bin's low pack_low_bits bits go into descriptor bits
+                               // 54.. (descriptors < 2^54, i.e. positions < 2^43)
 };
+constexpr int kDescPackShift = 54;
 cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t s);
 // Second level of a two-level scatter: descriptors already grouped by bin >> shift
 // (group g = [off[g << shift], off[min((g + 1) << shift, n_bins)]) of desc_in/bin_in)
 // are regrouped by bin inside each group with shared-memory cursors.
 cudaError_t launch_regroup_fine(const uint64_t* desc_in, const uint32_t* bin_in, const unsigned long long* off,
                                 uint32_t n_bins, uint32_t shift, uint64_t* desc_out, cudaStream_t s);
+// the same with the bin's low `shift` bits packed in the descriptors (ScatterArgs.pack_low_bits)
+cudaError_t launch_regroup_fine_packed(const uint64_t* desc_in, const unsigned long long* off, uint32_t n_bins,
+                                       uint32_t shift, uint64_t* desc_out, cudaStream_t s);
 
 // world > 1: copy every local super-mer (descriptor + word-aligned payload)
 // into the send buffer, ordered by (destination rank, bin).

@@ -57,8 +57,13 @@ scatter_smem_kernel(ScatterArgs a, uint64_t n_chunks) {
     for (int j = 0; j < kPer; ++j)
       if (bins[j] != 0xffffffffu) {
         const uint64_t d = s_base[bins[j]] + rank[j];
-        a.desc_out[d] = desc[j] + (a.pos_add << kNwinBits);
-        if (a.bin_out) a.bin_out[d] = a.bin_shift ? a.bin_in[i0 + j * kThreads + tid] : bins[j];
+        if (a.pack_low_bits) {  // one 8-byte store per descriptor: the fine bin rides in bits 54..
+          const uint32_t full = a.bin_in[i0 + j * kThreads + tid];
+          a.desc_out[d] = desc[j] | ((uint64_t)(full & ((1u << a.pack_low_bits) - 1u)) << kDescPackShift);
+        } else {
+          a.desc_out[d] = desc[j] + (a.pos_add << kNwinBits);
+          if (a.bin_out) a.bin_out[d] = a.bin_shift ? a.bin_in[i0 + j * kThreads + tid] : bins[j];
+        }
       }
     __syncthreads();
 #pragma unroll
@@ -127,7 +132,34 @@ __global__ void __launch_bounds__(kFineThreads) regroup_fine_kernel(const uint64
   }
 }
 
+__global__ void __launch_bounds__(kFineThreads) regroup_fine_packed_kernel(const uint64_t* __restrict__ desc_in,
+                                                                           const unsigned long long* __restrict__ off,
+                                                                           uint32_t n_bins, uint32_t shift,
+                                                                           uint64_t* __restrict__ desc_out) {
+  extern __shared__ uint32_t s_cur[];  // [1 << shift] cursors relative to the group's first descriptor
+  const uint32_t g = blockIdx.x, fan = 1u << shift, b0 = g << shift;
+  const uint32_t b1 = min(b0 + fan, n_bins);
+  const uint64_t i0 = off[b0], i1 = off[b1];
+  for (uint32_t t = threadIdx.x; t < fan; t += blockDim.x) s_cur[t] = b0 + t < b1 ? (uint32_t)(off[b0 + t] - i0) : 0u;
+  __syncthreads();
+  constexpr uint64_t kLow = (1ull << kDescPackShift) - 1;
+  for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint64_t d = desc_in[i];
+    const uint32_t p = atomicAdd(&s_cur[(uint32_t)(d >> kDescPackShift)], 1u);
+    desc_out[i0 + p] = d & kLow;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_regroup_fine_packed(const uint64_t* desc_in, const unsigned long long* off, uint32_t n_bins,
+                                       uint32_t shift, uint64_t* desc_out, cudaStream_t st) {
+  const uint32_t groups = (n_bins + (1u << shift) - 1) >> shift;
+  if (groups == 0) return cudaSuccess;
+  regroup_fine_packed_kernel<<<groups, kFineThreads, (size_t)4 << shift, st>>>(desc_in, off, n_bins, shift,
+                                                                                desc_out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_regroup_fine(const uint64_t* desc_in, const uint32_t* bin_in, const unsigned long long* off,
                                 uint32_t n_bins, uint32_t shift, uint64_t* desc_out, cudaStream_t st) {
