@@ -399,13 +399,16 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
 
     if (f0 & 2u) {  // last chunk of the bin: output or abandon, clear the table
       if (!abandoned) {
-        uint32_t keep = 0;
-        for (uint32_t s = lane; s < cb; s += 32) {
-          const uint32_t n = T.count(s);
-          keep += n >= a.min_count ? 1u : 0u;
-        }
+        uint32_t keep = n_distinct;  // min_count 1: every occupied slot is output
+        if (a.min_count > 1) {
+          keep = 0;
+          for (uint32_t s = lane; s < cb; s += 32) {
+            const uint32_t n = T.count(s);
+            keep += n >= a.min_count ? 1u : 0u;
+          }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) keep += __shfl_xor_sync(kFull, keep, off);
+          for (int off = 16; off > 0; off >>= 1) keep += __shfl_xor_sync(kFull, keep, off);
+        }
         unsigned long long off = 0;
         if (lane == 0 && keep) off = atomicAdd(a.out_n, (unsigned long long)keep);
         off = __shfl_sync(kFull, off, 0);
