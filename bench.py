@@ -6,10 +6,11 @@ synthetic reads already resident in HBM, through the C ABI
 (gerbil_count_device). N=1 workload = BASELINE.json configs[1]: F. vesca-scale
 synthetic Illumina reads (5×10^7 × 100 bp = 5 Gbp), k=40, min_count=1; m=15 (results do
 not depend on m; m=15 makes ~4M bins small enough for the shared-memory count kernel).
-Under torchrun (N>1) every rank counts its own 5 Gbp shard (weak scaling) and
-bins are shuffled across ranks with NCCL.
+`--config C2|C3k65|C3k100|C4` runs the per-GPU shards of BASELINE configs[2..4]
+(synth/configs.py). Under torchrun (N>1) every rank counts its own shard (weak
+scaling) and bins are shuffled across ranks with NCCL.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config C1]
 
 Rank 0 prints ONE JSON line. `--impl reference` times the CPU oracle (the
 reference arm of this tier) on the host cores instead.
@@ -31,21 +32,26 @@ sys.path.insert(0, ROOT)
 METRIC = "input bases/s counted (k-mer counting phase, steps b-e)"
 UNIT = "bases/s"
 
-# configs[1]: "F. vesca-scale synthetic Illumina reads (~5 Gbp, 100-bp), k=40, 1xB200"
-C1 = dict(seed=2, genome_len=240_000_000, read_len=100, n_reads=50_000_000, err=0.0033, nrate=0.0001)
-K, M, MIN_COUNT = 40, 15, 1
-WORKLOAD_NAME = ""
+from synth.configs import CONFIGS  # noqa: E402  (workload recipes shared with the parity tests)
+
+# the driver's default: configs[1] "F. vesca-scale synthetic Illumina reads (~5 Gbp, 100-bp), k=40, 1xB200"
+CFG = CONFIGS["C1"]
+K, M, MIN_COUNT = CFG.k, CFG.m, CFG.min_count
+WORKLOAD_NAME = CFG.label()
+ORACLE_SAMPLE_BASES = 10_000_000  # per single-thread oracle step: ~10 s of std::map work
 
 
-def set_m(m: int) -> None:
-    global M, WORKLOAD_NAME
-    M = m
-    WORKLOAD_NAME = (f"C1: F. vesca-scale synthetic Illumina reads, 5e7 x 100 bp = 5 Gbp per GPU, k=40, m={m}, "
-                     "min_count=1")
+def set_config(name: str, m: int | None, n_reads: int | None) -> None:
+    global CFG, K, M, MIN_COUNT, WORKLOAD_NAME
+    CFG = CONFIGS[name]
+    K, M, MIN_COUNT = CFG.k, (m or CFG.m), CFG.min_count
+    WORKLOAD_NAME = CFG.label(n_reads).replace(f"m={CFG.m}", f"m={M}")
 
 
-set_m(M)
-ORACLE_SAMPLE_READS = 100_000  # 10 Mbp per oracle step: ~10 s of single-thread std::map work
+def oracle_sample_reads() -> int:
+    # ~10 s of single-thread std::map work: fewer bases for long keys (k=200 costs ~5x k=40 per window)
+    bases = ORACLE_SAMPLE_BASES * min(1.0, 40.0 / K)
+    return max(1, int(bases) // CFG.read_len)
 
 
 def _peaks():
@@ -121,16 +127,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _oracle_text(n_reads: int) -> tuple:
+    import synth
+
+    w = CFG.workload(min(n_reads, CFG.n_reads))
+    return w, synth.fastx(w, synth.FASTQ)
+
+
 def run_reference(args) -> None:
-    """Reference arm: the CPU oracle as it stands, on the host cores."""
+    """Reference arm: the CPU oracle as it stands (single thread), on the host cores, on a
+    bounded prefix of the same workload (SURVEY.md §8(d) "Oracle timing")."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    import synth
 
-    w = synth.Workload(**{**C1, "n_reads": ORACLE_SAMPLE_READS})
-    text = synth.fastx(w, synth.FASTQ)
+    n = oracle_sample_reads()
+    w, text = _oracle_text(n)
     for _ in range(args.warmup):
         oracle.count(text, K, MIN_COUNT)
     times = []
@@ -143,7 +156,8 @@ def run_reference(args) -> None:
     t = statistics.median(times)
     value = w.n_bases / t
     model, ncpu = _cpu_info()
-    sample = f"first {ORACLE_SAMPLE_READS} reads of C1 ({w.n_bases / 1e6:.0f} Mbp) per step, FASTQ text, single thread"
+    sample = (f"first {w.n_reads} reads of {CFG.name} ({w.n_bases / 1e6:.0f} Mbp) per step, FASTQ text, "
+              "single-thread std::map oracle")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -157,20 +171,128 @@ def run_reference(args) -> None:
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline() -> dict:
+def cpu_baseline(full_reads: int, full: bool) -> dict:
+    """The oracle timed on the box's host cores (SURVEY.md §8(d)): (1) single-thread std::map
+    oracle on a bounded prefix of the workload; (2) the hash-sampled oracle (oracle_count_sampled,
+    keeps canonical k-mers with FNV-1a % 4096 == 0) over the FULL per-GPU input on all cores."""
     import oracle
-    import synth
 
-    w = synth.Workload(**{**C1, "n_reads": ORACLE_SAMPLE_READS})
-    text = synth.fastx(w, synth.FASTQ)
+    n = oracle_sample_reads()
+    w, text = _oracle_text(n)
     t0 = time.perf_counter()
     r = oracle.count(text, K, MIN_COUNT)
     t = time.perf_counter() - t0
+    del text
     model, ncpu = _cpu_info()
-    return {"value": w.n_bases / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {ORACLE_SAMPLE_READS} reads of C1 ({w.n_bases / 1e6:.0f} Mbp), k={K}, "
-                      f"single-thread std::map oracle, {t:.1f} s", "kmers_per_s": r.windows / t,
-            "cpu": model, "host_cores": ncpu}
+    out = {"value": w.n_bases / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"first {w.n_reads} reads of {CFG.name} ({w.n_bases / 1e6:.0f} Mbp), k={K}, "
+                     f"single-thread std::map oracle, {t:.1f} s", "kmers_per_s": r.windows / t,
+           "cpu": model, "host_cores": ncpu}
+    if full:
+        import synth
+
+        wf = CFG.workload(full_reads)
+        t0 = time.perf_counter()
+        txt = synth.fastx(wf, synth.FASTA)
+        tg = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rs = oracle.count_sampled(txt, K, MIN_COUNT, mod=4096, threads=0)
+        ts = time.perf_counter() - t0
+        del txt
+        out["sampled_full"] = {
+            "value": wf.n_bases / ts, "unit": UNIT, "cores": ncpu, "kind": "oracle_count_sampled",
+            "kmers_per_s": rs.windows / ts, "seconds": ts, "text_gen_seconds": tg,
+            "sample": f"all {wf.n_reads} reads ({wf.n_bases / 1e9:.2f} Gbp) of the timed workload, every valid "
+                      f"window canonicalised, only k-mers with FNV-1a-64 % 4096 == 0 kept in the std::map, "
+                      f"{ncpu} threads", "windows": rs.windows, "kept_sampled": len(rs.kmers)}
+    return out
+
+
+def slot_bytes(W: int) -> int:
+    """table slot S = 8W+4 (W=1) or 8W+8 (W>1, with tag)."""
+    return 8 * W + 4 if W == 1 else 8 * W + 8
+
+
+def stream_model(st: dict, k: int, P: int, alpha: float = 0.7) -> dict:
+    """SURVEY.md §8(d) algorithmic bytes of one step (per GPU):
+    0.25 b + 2 (1 + (P-1)/P) (0.25 E b + 8 n_s) + 2 S d / alpha + (8W+4) d_kept; random-sector
+    model adds 64 n_k. E b = super-mer bases = n_k + n_s (k-1)."""
+    b, n_k, n_s = float(st["input_bases"]), float(st["valid_windows"]), float(st["supermers"])
+    d, d_kept, W = float(st["distinct"]), float(st["kept"]), int(st["W"])
+    S = slot_bytes(W)
+    eb = n_k + n_s * (k - 1)
+    terms = {"reads": 0.25 * b, "supermers": 2 * (1 + (P - 1) / P) * (0.25 * eb + 8 * n_s),
+             "table": 2 * S * d / alpha, "output": (8 * W + 4) * d_kept}
+    stream = sum(terms.values())
+    return {"terms": terms, "stream": stream, "random": stream + 64 * n_k, "S": S, "alpha": alpha,
+            "supermer_bases": eb,
+            # steps (d)+(e) alone: read super-mers + descriptors back, table init + scan, output
+            "count_bytes": 0.25 * eb + 8 * n_s + terms["table"] + terms["output"]}
+
+
+def _traffic_table() -> dict:
+    out = {}
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        for e in (tj if isinstance(tj, list) else [tj]):
+            if e.get("workload") == WORKLOAD_NAME:
+                out[e.get("kernel")] = e
+    return out
+
+
+def roofline_report(st: dict, ms: float, per_kernel: dict, steps: int, P: int) -> dict:
+    peak, peak_src = _peaks()
+    model = stream_model(st, K, P)
+    traffic = _traffic_table()
+    n_k = max(float(st["valid_windows"]), 1.0)
+    smem_share = st["smem_windows"] / n_k
+    if smem_share >= 0.5:
+        kname, key, launches, kms = "count_smem_kernel", "smem", st["launches_smem"], per_kernel["smem"][0] / steps
+        units = float(st["smem_windows"])
+    else:
+        kname, key, launches, kms = "count_inline_kernel", "count", st["launches_count"], per_kernel["count"][0] / steps
+        units = n_k
+    # SURVEY.md §8(d) per-window bytes of steps (d)+(e) x the windows this kernel's launches counted
+    per_window = model["count_bytes"] / n_k
+    bytes_step = per_window * units
+    achieved = bytes_step / (kms / 1e3) / 1e9 if kms > 0 else None
+    tr = traffic.get(kname, {})
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": tr.get("dram_bytes_per_launch"), "peak_source": peak_src,
+            "bytes_model": "SURVEY.md §8(d) steps (d)+(e): (0.25*supermer_bases + 8*supermers + 2*S*distinct/alpha "
+                           f"+ {8 * int(st['W']) + 4}*kept) / windows, S={model['S']}, alpha={model['alpha']}; "
+                           "x windows this kernel counted",
+            "bytes_per_window": per_window, "algorithmic_bytes_per_launch": bytes_step / max(launches, 1),
+            "avg_launch_ms": kms / max(launches, 1), "launches_per_step": launches,
+            "share_of_step": kms / ms if ms > 0 else None, "windows_share": units / n_k,
+            "traffic_source": tr.get("source")}
+    # the whole step against the §8(d) stream model (the north star's "fraction of the HBM roofline")
+    t = model["terms"]
+    roof["step"] = {
+        "bound": "hbm", "unit": "GB/s", "peak": peak,
+        "algorithmic_bytes": model["stream"], "achieved": model["stream"] / (ms / 1e3) / 1e9,
+        "frac": model["stream"] / (ms / 1e3) / 1e9 / peak,
+        "terms_gb": {x: v / 1e9 for x, v in t.items()},
+        "floor_ms_stream": model["stream"] / (peak * 1e9) * 1e3,
+        "floor_ms_random_sector": model["random"] / (peak * 1e9) * 1e3,
+        "frac_of_random_sector_floor": (model["random"] / (peak * 1e9) * 1e3) / ms,
+        "model": "SURVEY.md §8(d) stream model: 0.25b + 2(1+(P-1)/P)(0.25Eb + 8n_s) + 2Sd/alpha + (8W+4)d_kept; "
+                 "random-sector model adds 64 n_k"}
+    # what actually binds the shared-memory kernel: instruction issue (ncu)
+    if kname == "count_smem_kernel" and tr.get("warp_inst_per_step"):
+        sms, clk = 148, tr.get("sm_mhz", 1965.0) * 1e6
+        wi = float(tr["warp_inst_per_step"])
+        roof["issue"] = {
+            "bound": "issue", "unit": "warp-inst/s", "warp_inst_per_window": wi / max(units, 1.0),
+            "warp_inst_per_round_of_32": 32 * wi / max(units, 1.0),
+            "achieved": wi / (kms / 1e3) if kms > 0 else None, "peak": 4 * sms * clk,
+            "frac": (wi / (kms / 1e3)) / (4 * sms * clk) if kms > 0 else None,
+            "ipc_ncu": tr.get("ipc"), "issue_slots_busy_ncu": tr.get("issue_slots_busy"),
+            "source": tr.get("source"),
+            "note": "4 warp-instructions per cycle per SM x 148 SMs x SM clock (B200_PROFILING.md)"}
+    return roof
 
 
 def main() -> None:
@@ -179,21 +301,23 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--reads", type=int, default=C1["n_reads"], help="reads per GPU (default: C1)")
+    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS),
+                    help="workload (synth/configs.py); C1 = BASELINE configs[1], the driver default")
+    ap.add_argument("--reads", type=int, default=0, help="reads per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-full", action="store_true", help="skip the all-core sampled oracle over the full input")
     ap.add_argument("--table-mb", type=int, default=0)
-    ap.add_argument("--bins", type=int, default=0)
-    ap.add_argument("--m", type=int, default=M, help="minimizer length (results are invariant in m)")
+    ap.add_argument("--bins", type=int, default=-1)
+    ap.add_argument("--m", type=int, default=0, help="minimizer length (results are invariant in m)")
     ap.add_argument("--count-mode", type=int, default=0, help="gerbil_config.count_mode (0 auto, 1 L2, 2 smem)")
     args = ap.parse_args()
-    set_m(args.m)
+    set_config(args.config, args.m or None, args.reads or None)
     if args.impl == "reference":
         run_reference(args)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -214,14 +338,13 @@ def main() -> None:
         obj = [gerbil.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    # N > 1: ranks need the same explicit B; the multi-rank plan (LPT over all bins) runs on the
-    # host, so keep B moderate there (L2 wave tables); N = 1 lets the library pick (4M bins, m = 15)
-    n_bins = args.bins or (4096 if world > 1 else 0)
+    n_bins = CFG.n_bins if args.bins < 0 else args.bins
     g = gerbil.Gerbil(device=local, rank=rank, world=world, unique_id=uid, n_bins=n_bins,
                       stream=stream.cuda_stream, timing=True,
                       wave_table_bytes=args.table_mb << 20, count_mode=args.count_mode)
 
-    w = synth.Workload(**{**C1, "n_reads": args.reads, "first_read": rank * args.reads})
+    n_reads = args.reads or CFG.n_reads
+    w = CFG.workload(n_reads, rank=rank)
     codes, nmask, rs = synth.packed_device(w, device=dev, stream=stream.cuda_stream)
     torch.cuda.synchronize(dev)
 
@@ -272,80 +395,7 @@ def main() -> None:
     else:
         total_bases, total_windows = float(st["input_bases"]), float(st["valid_windows"])
     value = total_bases / (ms / 1e3)
-
-    # ---- roofline of the dominant kernel (count, step d) ----------------------------------
-    peak, peak_src = _peaks()
-    W = st["W"]
-    sm_bases = st["valid_windows"] + st["supermers"] * (K - 1)
-    traffic_tbl = {}
-    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tpath):
-        tj = json.load(open(tpath))
-        for e in (tj if isinstance(tj, list) else [tj]):
-            if e.get("workload") == WORKLOAD_NAME:
-                traffic_tbl[e.get("kernel")] = e
-    smem_share = st["smem_windows"] / max(st["valid_windows"], 1)
-    if smem_share >= 0.5:
-        # step (d)+(e) in per-warp shared-memory tables (count_smem.cu): per window, the
-        # algorithmic HBM bytes are the descriptor (8 B/super-mer) and packed bases (0.25 B/base)
-        # it reads and the (8W+4)-byte (k-mer, count) pair it writes per kept k-mer; the table
-        # lives in shared memory. Units per launch = the windows it counted.
-        n_smem = max(per_kernel["smem"][1], 1)
-        avg_ms = per_kernel["smem"][0] / n_smem
-        per_window = (8 * st["supermers"] + 0.25 * sm_bases + (8 * W + 4) * st["kept"]) / max(st["valid_windows"], 1)
-        bytes_per_launch = per_window * st["smem_windows"] / max(st["launches_smem"], 1)
-        achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else None
-        kname = "count_smem_kernel<2,true>"
-        tr = traffic_tbl.get("count_smem_kernel", {})
-        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": (achieved / peak) if achieved else None,
-                    "traffic": tr.get("dram_bytes_per_launch"), "peak_source": peak_src,
-                    "bytes_model": f"per window: (8*supermers + 0.25*supermer_bases + {8 * W + 4}*kept) / windows; "
-                                   "x windows counted in shared memory per launch",
-                    "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
-                    "launches_per_step": st["launches_smem"],
-                    "share_of_step": per_kernel["smem"][0] / args.steps / ms,
-                    "windows_share": smem_share,
-                    "issue_slot_util": tr.get("issue_slots_busy"),
-                    "note": "table in shared memory: the kernel is bound by instruction issue and "
-                            "shared-memory latency (ncu issue_slot_util), not HBM; DESIGN.md §4"}
-    else:
-        # table bytes per slot: 16 B inline slots for k <= 46, else the chunked bucket / 4
-        slot = 16 if K <= 46 else (32 + 32 * ((K + 30) // 31)) / 4
-        n_count = max(per_kernel["count"][1], 1)
-        avg_count_ms = per_kernel["count"][0] / n_count
-        # algorithmic bytes per step of the count kernel (SURVEY.md §8(d) stream model restricted to
-        # this kernel): descriptors (8 B/super-mer), packed super-mer bases
-        # (0.25 B/base), and one write of every claimed table slot (slot B per distinct k-mer).
-        count_bytes_step = 8 * st["supermers"] + 0.25 * sm_bases + slot * st["distinct"]
-        bytes_per_launch = count_bytes_step / max(st["launches_count"], 1)
-        achieved = bytes_per_launch / (avg_count_ms / 1e3) / 1e9 if avg_count_ms > 0 else None
-        tr = traffic_tbl.get("count_inline_kernel", {})
-        roofline = {"bound": "hbm", "kernel": "count_inline_kernel<2,true>", "achieved": achieved, "peak": peak,
-                    "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                    "traffic": tr.get("dram_bytes_per_launch"), "peak_source": peak_src,
-                    "bytes_model": f"8*supermers + 0.25*supermer_bases + {slot:g}*distinct per step",
-                    "algorithmic_bytes_per_launch": bytes_per_launch,
-                    "avg_launch_ms": avg_count_ms, "launches_per_step": st["launches_count"],
-                    "share_of_step": per_kernel["count"][0] / args.steps / ms,
-                    "note": "L2-resident table: the kernel is bound by the L2 random-access rate of its "
-                            "bucket-load + atomic pattern, not HBM; see l2_ceiling and DESIGN.md §4"}
-        # The bound that applies: one 64-byte bucket load + one atomic into the same bucket per window
-        # (RED for a k-mer already present, 128-bit CAS for a new one). scripts/l2_micro.cu measured
-        # what B200's L2 sustains for these patterns on a 64 MiB table (profiles/r01_l2_micro.txt).
-        L2_LOAD_RED, L2_LOAD_CAS = 49.2e9, 38.3e9  # ops/s, "load+red" / "load+cas" rows
-        new_k = float(st["distinct"])
-        hits = max(float(st["valid_windows"]) - new_k, 0.0)
-        t_floor = hits / L2_LOAD_RED + new_k / L2_LOAD_CAS
-        d_ms = per_kernel["count"][0] / args.steps  # steps (d)+(e) device time per step
-        roofline["l2_ceiling"] = {
-            "bound": "l2_random_ops", "unit": "G window-ops/s",
-            "achieved": float(st["valid_windows"]) / (d_ms / 1e3) / 1e9 if d_ms > 0 else None,
-            "peak": float(st["valid_windows"]) / t_floor / 1e9 if t_floor > 0 else None,
-            "frac": (t_floor * 1e3 / d_ms) if d_ms > 0 else None,
-            "floor_ms": t_floor * 1e3, "measured_ms": d_ms,
-            "source": "profiles/r01_l2_micro.txt (load+red 49.2, load+cas 38.3 Gop/s, 64 MiB table); "
-                      "measured_ms = steps (d)+(e) incl. compaction"}
+    roofline = roofline_report(st, ms, per_kernel, args.steps, world)
 
     # ---- end to end through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -382,21 +432,23 @@ def main() -> None:
             te = float(t.item())
         e2e = {"value": total_bases / te, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": te * 1e3,
-               "stage_ms": {x: est["ms_" + x] for x in ("h2d", "supermer", "shuffle", "count", "compact")},
+               "stage_ms": {x: est["ms_" + x] for x in ("h2d", "supermer", "shuffle", "count", "smem", "compact")},
+               "smem_windows_share": est["smem_windows"] / max(est["valid_windows"], 1),
                "path": "gerbil_count_host_stream: pinned H2D of the packed batch, steps (b)-(e), and every "
-                       "(k-mer, count) as the paper's binary record (App. C) streamed to pinned host memory by "
-                       "the compaction kernel while later waves are counted; wall clock per call, max over ranks"}
+                       "(k-mer, count) as the paper's binary record (App. C) streamed to pinned host memory "
+                       "while later bins are counted; wall clock per call, max over ranks"}
+        del hc, hn, hr, rec
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64 (2-bit packed k-mer words, u32 counts)", "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAME, "reads_per_gpu": w.n_reads, "read_len": w.read_len,
-                       "genome_len": w.genome_len, "err": w.err, "nrate": w.nrate, "k": K, "m": M,
-                       "min_count": MIN_COUNT, "n_bins": st["n_bins"], "waves": st["waves"],
+            "config": {"workload": WORKLOAD_NAME, "config": CFG.name, "reads_per_gpu": w.n_reads,
+                       "read_len": w.read_len, "genome_len": w.genome_len, "err": w.err, "nrate": w.nrate,
+                       "k": K, "m": M, "min_count": MIN_COUNT, "n_bins": st["n_bins"], "waves": st["waves"],
                        "parallelism": f"bins sharded over {world} GPU(s)",
-                       "l2": "inputs larger than L2 (packed reads 1.25 GB/GPU); no flush"},
+                       "l2": "inputs larger than L2 (packed reads >= 1.25 GB/GPU); no flush"},
             "kmers_per_s": total_windows / (ms / 1e3),
             "stage_ms": {"supermer": per_kernel["supermer"][0] / args.steps,
                          "shuffle": per_kernel["shuffle"][0] / args.steps,
@@ -416,7 +468,9 @@ def main() -> None:
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:
-            out["cpu_baseline"] = cpu_baseline()
+            del codes, nmask, rs
+            g.close()
+            out["cpu_baseline"] = cpu_baseline(n_reads, not args.no_cpu_full)
         print(json.dumps(out), flush=True)
     g.close()
     if world > 1:

@@ -94,7 +94,9 @@ typedef struct {
                               nccl_unique_id = any 128-byte group key) */
   uint32_t n_bins;         /* B (temporary-file analogue, PAPER.md:459 `-f`); 0 = auto (>= 512) */
   int32_t ordering;        /* gerbil_ordering; 0 = KMC2 */
-  uint64_t device_mem_cap; /* bytes of device memory the library may allocate; 0 = auto (`-e`) */
+  uint64_t device_mem_cap; /* out-of-core budget (`-e`): gerbil_spill_finish counts bin
+                             groups of at most device_mem_cap / 2 bytes of super-mers; 0 = 16 GiB groups.
+                             The in-core calls size their buffers from the input and do not read it. */
   int32_t host_threads;    /* host reader threads; 0 = all cores (`-t`) */
   uint32_t max_probes;     /* θ in buckets; 0 = 32; capped at 2^20 */
   double distinct_ratio;   /* initial ρ̂ = distinct/total estimate; 0 = 0.5 */
@@ -283,7 +285,10 @@ gerbil_status gerbil_count_text(gerbil_ctx* ctx, const char* text, uint64_t len,
  * super-mers from every batch are uploaded, regrouped by bin and counted
  * (steps d, e) — and streams the App. C records of every k-mer with count
  * >= min_count into out (page-locked, as gerbil_count_host_stream; capacity 0
- * = sizing: *n_bytes is the size needed, GERBIL_E_USAGE). The histogram is
+ * = sizing: *n_bytes is the size needed, GERBIL_E_USAGE). A sizing call, or a
+ * buffer that is too small, keeps the spilled job: call gerbil_spill_finish
+ * again with a buffer of *n_bytes (phase one is not repeated); a successful
+ * call or any other error ends the job. The histogram is
  * the same as one gerbil_count over the concatenated batches. No device
  * result set remains (gerbil_fetch → GERBIL_E_STATE); stats describe the whole
  * job. One rank only; the DFP ordering is refused (its table is per batch).

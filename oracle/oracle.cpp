@@ -454,8 +454,10 @@ uint32_t oracle_order_key(const char* mmer, uint32_t m, int ordering, const uint
  *             one read with no undetermined base; each occurrence counts
  *             for f and for rc(f);
  *  position = rank in ascending (frequency, A<C<G<T number) order;
- *  P        = min(4^m - 1, floor(p * 4^m));
- *  key      = 2 (pos - P) when pos >= P, else 2 (P - pos) - 1.
+ *  key      = rank of the position in ascending (|position - 4^m p|,
+ *             position) order: the pivot 4^m p is the real number the paper
+ *             names, and equal distances go to the smaller initial position
+ *             (SPEC.md:196, :176).
  * Writes 4^m keys (index = the A<C<G<T number); returns 0, or -1 on a parse error. */
 int oracle_dfp_table(const char* text, uint64_t len, uint32_t m, double pivot, uint32_t stride,
                      uint32_t* out) {
@@ -483,9 +485,14 @@ int oracle_dfp_table(const char* text, uint64_t len, uint32_t m, double pivot, u
   std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     return freq[a] != freq[b] ? freq[a] < freq[b] : a < b;
   });
-  const uint64_t P = std::min<uint64_t>(M - 1, (uint64_t)std::floor(pivot * (double)M));
-  for (uint64_t pos = 0; pos < M; ++pos)
-    out[order[pos]] = (uint32_t)(pos >= P ? 2 * (pos - P) : 2 * (P - pos) - 1);
+  const double x = pivot * (double)M; /* the pivot position 4^m p */
+  std::vector<uint64_t> bypiv(M);
+  for (uint64_t pos = 0; pos < M; ++pos) bypiv[pos] = pos;
+  std::sort(bypiv.begin(), bypiv.end(), [&](uint64_t a, uint64_t b) {
+    const double da = std::fabs((double)a - x), db = std::fabs((double)b - x);
+    return da != db ? da < db : a < b;
+  });
+  for (uint64_t r = 0; r < M; ++r) out[order[bypiv[r]]] = (uint32_t)r;
   return 0;
 }
 

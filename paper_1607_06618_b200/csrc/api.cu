@@ -450,7 +450,7 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
   const uint32_t W = key_words(k);
   const uint64_t bb = table_inline(k) ? kInlineBucketBytes : table_bucket_bytes(k);
   const double slot_bytes = (double)bb / kSlotsPerBucket;
-  const double alpha = ctx->cfg.target_load;
+  double alpha = ctx->cfg.target_load;  // lowered on a retry once rho can grow no further
   const uint32_t theta = std::min<uint32_t>(ctx->cfg.max_probes, 1u << 20);  // probe counters are 24-bit
   const int lanes = wave_lanes();
   const double budget = (double)ctx->cfg.wave_table_bytes / lanes;  // per-lane table bytes
@@ -674,6 +674,9 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
         host_off = ctx->rec_base;
       }
       ctx->rho = std::min(1.0, std::max(2.0 * rho, 1.25 * observed + 0.02));
+      // rho is capped at 1 (distinct <= windows): with alpha > 1 the tables would keep their
+      // size on every retry, so shrink the load target instead
+      if (ctx->rho <= rho && alpha > 0.5) alpha = std::max(0.5, alpha * 0.5);
       if (attempt > 8) return fail(ctx, GERBIL_E_INTERNAL, "table sizing did not converge");
       continue;
     }
@@ -842,7 +845,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
         r2[2 * n2 + 1] = rb.d1 | (std::min<uint64_t>(rb.win, (1u << 24) - 1) << kRangeWinShift);
         ++n2;
         w2 += rb.win;
-        ob2 += std::min<uint64_t>(rb.win, mf2);
+        ob2 += smem_bin_out_bound(rb.win, cap2, mf2);
       } else {
         keep.push_back(rb);
       }
@@ -980,7 +983,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
     const uint32_t b = elig[i];
     rng[2 * i] = bin_off[b];
     rng[2 * i + 1] = bin_off[b + 1] | (std::min<uint64_t>(bin_win[b], (1u << 24) - 1) << kRangeWinShift);
-    out_bound += std::min<uint64_t>(bin_win[b], max_fill);
+    out_bound += smem_bin_out_bound(bin_win[b], cap, max_fill);
     elig_windows += bin_win[b];
   }
   CK(ctx->smem_range.ensure(2 * (size_t)n * 8));
@@ -1050,6 +1053,7 @@ gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, ui
   pa.n_bins = B;
   pa.thr = smem_window_threshold(ctx, max_fill);
   pa.max_fill = max_fill;
+  pa.cap = cap;
   pa.elig = ctx->smem_range.as<unsigned long long>();
   pa.rest = ctx->rest_range.as<unsigned long long>();
   pa.sums = ctx->plan_sums.as<unsigned long long>();
@@ -1126,9 +1130,17 @@ gerbil_status build_dfp_table(gerbil_ctx* ctx, const SupermerArgs& a, uint64_t n
   std::vector<uint32_t> order(M);
   std::iota(order.begin(), order.end(), 0u);
   std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return f[x] != f[y] ? f[x] < f[y] : x < y; });
-  const uint64_t P = std::min<uint64_t>(M - 1, (uint64_t)std::floor(ctx->cfg.dfp_pivot * (double)M));
+  // re-sort by |position - 4^m p| (the real pivot; p * 4^m is exact in double), ties to the
+  // smaller position (Q23); the key is the rank in that order
+  const double x = ctx->cfg.dfp_pivot * (double)M;
+  std::vector<uint32_t> bypiv(M);
+  std::iota(bypiv.begin(), bypiv.end(), 0u);
+  std::sort(bypiv.begin(), bypiv.end(), [&](uint32_t a, uint32_t b) {
+    const double da = std::fabs((double)a - x), db = std::fabs((double)b - x);
+    return da != db ? da < db : a < b;
+  });
   std::vector<uint32_t> key(M);
-  for (uint64_t pos = 0; pos < M; ++pos) key[order[pos]] = (uint32_t)(pos >= P ? 2 * (pos - P) : 2 * (P - pos) - 1);
+  for (uint64_t r = 0; r < M; ++r) key[order[bypiv[r]]] = (uint32_t)r;
   CK(cudaMemcpyAsync(ctx->order_rank.p, key.data(), M * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));  // key is a host temporary
   return GERBIL_OK;
@@ -2099,8 +2111,10 @@ gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* 
   const uint64_t total = ctx->rec_base;
   ctx->rec_base = 0;
   ctx->have_result = false;  // results were streamed group by group; no device-resident set remains
-  sp.release();
-  if (st != GERBIL_OK) return st;
+  if (st != GERBIL_OK) {
+    sp.release();
+    return st;
+  }
   ctx->stats.input_bases = sp.bases;
   ctx->stats.input_reads = sp.reads;
   ctx->stats.valid_windows = sp.windows;
@@ -2114,11 +2128,16 @@ gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* 
   ctx->stats.n_bins = B;
   ctx->stats.W = ctx->W;
   *n_bytes = total;
-  if (count_sum != sp.windows)
+  if (count_sum != sp.windows) {
+    sp.release();
     return fail(ctx, GERBIL_E_INTERNAL, "invariant violated: sum of counts != valid windows");
+  }
+  // a sizing call (capacity 0) or a too-small buffer keeps the spilled job: call again with
+  // a buffer of *n_bytes (phase one is not repeated)
   if (total > capacity)
     return fail(ctx, GERBIL_E_USAGE, "output capacity " + std::to_string(capacity) + " < " +
                                          std::to_string(total) + " record bytes");
+  sp.release();
   return GERBIL_OK;
 }
 

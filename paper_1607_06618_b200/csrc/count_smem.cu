@@ -205,9 +205,7 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
     const uint64_t b0 = wd0 + wc * 32;
     uint32_t f = 4u | (wc == 0 ? 1u : 0u) | (b0 + 32 >= e ? 2u : 0u);
     // slots for this bin: distinct <= windows, so a table of windows + 1/4 + 32 never fills
-    const uint32_t win = (uint32_t)(wd1 >> kRangeWinShift);
-    const uint32_t want = (win + (win >> 2) + 32u + 31u) & ~31u;
-    f |= (want < cap && !(a.dbg & 8u) ? want : cap) << 8;
+    f |= ((a.dbg & 8u) ? cap : smem_bin_slots(wd1 >> kRangeWinShift, cap)) << 8;
     if (b0 + lane < e) d = __ldg(a.desc + b0 + lane);
     if (f & 2u) {
       wi += G;
@@ -556,7 +554,7 @@ __global__ void plan_bins_kernel(PlanBinsArgs a) {
     }
     const bool el = has && w <= a.thr, rs = has && !el;
     const uint32_t me = __ballot_sync(kFull, el), mr = __ballot_sync(kFull, rs);
-    unsigned long long we = el ? w : 0ull, wf = el ? (w < a.max_fill ? w : (unsigned long long)a.max_fill) : 0ull,
+    unsigned long long we = el ? w : 0ull, wf = el ? smem_bin_out_bound(w, a.cap, a.max_fill) : 0ull,
                        wm = has ? w : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

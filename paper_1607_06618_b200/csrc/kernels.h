@@ -166,6 +166,18 @@ struct SmemCountArgs {
   uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 4 = no tag fast path
   int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match
 };
+// Table slots a bin of `win` windows gets (count_smem_kernel): windows * 1.25 + 32, rounded up to 32,
+// capped at the warp's table (cap).
+__host__ __device__ inline uint32_t smem_bin_slots(uint64_t win, uint32_t cap) {
+  const uint64_t w = win < (1ull << 24) ? win : (1ull << 24) - 1;
+  const uint64_t want = (w + (w >> 2) + 32u + 31u) & ~31ull;
+  return want < cap ? (uint32_t)want : cap;
+}
+// Output bound of one bin in the shared-memory pass: a bin with a full-size table is abandoned
+// past max_fill distinct k-mers (no output); a smaller table is never abandoned (distinct <= windows).
+__host__ __device__ inline uint64_t smem_bin_out_bound(uint64_t win, uint32_t cap, uint32_t max_fill) {
+  return smem_bin_slots(win, cap) < cap ? win : (win < max_fill ? win : max_fill);
+}
 int smem_count_warps(uint32_t k);                            // warps per CTA (GERBIL_SMEM_WARPS overrides)
 uint32_t smem_slot_bytes(uint32_t k);
 uint32_t smem_warp_bytes(uint32_t k, uint32_t cap);
@@ -176,10 +188,10 @@ struct PlanBinsArgs {
   const unsigned long long* off;   // [n_bins + 1] first descriptor of each bin (exclusive scan)
   uint32_t n_bins;
   unsigned long long thr;          // shared-memory list iff windows <= thr
-  uint32_t max_fill;
+  uint32_t cap, max_fill;          // table slots per warp, abandonment threshold (output bound)
   unsigned long long* elig;        // [n_bins][2] shared-memory list (range entries, kRangeWinShift)
   unsigned long long* rest;        // [n_bins][3] first descriptor, end descriptor, windows
-  unsigned long long* sums;        // [4]: n_elig, Σ elig windows, Σ min(windows, max_fill), n_rest (zeroed)
+  unsigned long long* sums;        // [4]: n_elig, Σ elig windows, Σ smem_bin_out_bound, n_rest (zeroed)
   unsigned long long* max_win;     // (zeroed)
 };
 cudaError_t launch_plan_bins(const PlanBinsArgs& a, int sms, cudaStream_t s);

@@ -61,10 +61,11 @@ def _spill(G, texts, k, m=7, min_count=1, **kw):
             need = 0
         except G.GerbilError as e:
             need = e.needed_bytes
-        # sizing consumed the spill: run again for the bytes
-        g.spill_begin(k, m)
-        for p in packs:
-            g.spill_add(p.codes, p.nmask, p.read_start, p.n_reads)
+        # the sizing call keeps the spilled job: a too-small buffer keeps it as well
+        if need > 1:
+            with pytest.raises(G.GerbilError) as e:
+                g.spill_finish(min_count, out=_pinned(need - 1))
+            assert e.value.status == G.E_USAGE and e.value.needed_bytes == need
         out = _pinned(need)
         n = g.spill_finish(min_count, out=out)
         st = g.stats()

@@ -385,19 +385,27 @@ def test_random_ordering_is_a_bijection():
 def test_dfp_table_planted_frequencies():
     # m = 1, text AAAAC: occurrences count for f and rc(f) → freq A = T = 4, C = G = 1.
     # ascending (freq, A<C<G<T) order: C, G, A, T → positions C0 G1 A2 T3.
-    t = list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.5, 1))   # P = 2: A→0, T→2, G→1, C→3
+    # key = rank by (|position - 4^m p|, position) (ties: smaller position)
+    t = list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.5, 1))   # pivot 2: A(2)→0, G(1)→1, T(3)→2, C(0)→3
     assert t == [0, 3, 1, 2]
-    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.0, 1)) == [4, 0, 2, 6]  # P = 0: key = 2·pos
-    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 1.0, 1)) == [1, 5, 3, 0]  # P = 3
+    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.0, 1)) == [2, 0, 1, 3]  # pivot 0: key = position
+    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 1.0, 1)) == [1, 3, 2, 0]  # pivot 4: key = 3 - position
+    # a pivot between positions: p = 0.3 → 4^m p = 1.2: positions 1 (0.2), 2 (0.8), 0 (1.2), 3 (1.8)
+    assert list(oracle.dfp_table(b">a\nAAAAC\n", 1, 0.3, 1)) == [1, 2, 0, 3]  # A=pos2, C=pos0, G=pos1, T=pos3
+    # (SPEC.md:176's example, positions T0 C1 G2 A3 with pivot 2 → G0 C1 A2 T3, is the same rule; its
+    # one-strand counts cannot be planted here because every occurrence also counts for rc(f).)
     # sampling: stride 2 samples tile 0 (positions 0..1023) only
     text = b">a\n" + b"A" * 1024 + b"C" * 1024 + b"\n"
     t2 = list(oracle.dfp_table(text, 1, 0.0, 2))  # freq A = T = 1024, C = G = 0 → C0 G1 A2 T3
-    assert t2 == [4, 0, 2, 6]
+    assert t2 == [2, 0, 1, 3]
     t1 = list(oracle.dfp_table(text, 1, 0.0, 1))  # all: A = T = C = G = 1024 → A0 C1 G2 T3
-    assert t1 == [0, 2, 4, 6]
+    assert t1 == [0, 1, 2, 3]
     # N and read ends break m-mers: "AN" and a 1-base read give no 2-mer
     t3 = list(oracle.dfp_table(b">a\nAN\n>b\nC\n", 2, 0.0, 1))
-    assert t3 == [2 * i for i in range(16)]  # all frequencies 0 → lexicographic positions
+    assert t3 == list(range(16))  # all frequencies 0 → lexicographic positions
+    # a pivot in the middle of 16 positions with equal distances: 4^2 * 0.5 = 8 → 8, 7, 9, 6, 10, ...
+    t4 = list(oracle.dfp_table(b">a\nAN\n", 2, 0.5, 1))
+    assert [t4.index(r) for r in range(16)] == [8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15, 0]
 
 
 def test_minimizer_stats_by_hand():
