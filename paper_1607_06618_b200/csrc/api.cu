@@ -1001,45 +1001,33 @@ gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, ui
                                       uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows,
                                       uint64_t n_bases) {
   ctx->stats.smem_slots = cap;
-  const unsigned long long* d_win = ctx->hist.as<unsigned long long>();
-  const unsigned long long* d_cnt = d_win + B;
+  (void)n_bases;
+  if (n_sm >= (1ull << 32))
+    return fail(ctx, GERBIL_E_USAGE, "more than 2^32 super-mers in one call: split the batch");
+  // (c): group-major shuffle (shuffle.cu) — bins' offsets and windows come out of it
+  unsigned long long* d_win = ctx->hist.as<unsigned long long>();
   CK(ctx->bin_off_d.ensure(((size_t)B + 1) * 8));
-  CK(ctx->p_tmp.ensure(scan_tmp_words(B) * 8));
   unsigned long long* d_off = ctx->bin_off_d.as<unsigned long long>();
-  CK(launch_scan_u64(reinterpret_cast<const uint64_t*>(d_cnt), reinterpret_cast<uint64_t*>(d_off), B,
-                     ctx->p_tmp.as<uint64_t>(), reinterpret_cast<uint64_t*>(d_off + B), ctx->stream));
   CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n_sm, 1) * 8));
-  // two-level counting sort: by bin >> kFineShift (shared-memory scatter), then by bin
-  // inside each group (shared-memory cursors, the group's output range stays in L2)
-  constexpr uint32_t kFineShift = 10;
-  const uint32_t groups = ((B - 1) >> kFineShift) + 1;
-  CK(ctx->cursor.ensure((size_t)groups * 8));
-  CK(cudaMemcpy2DAsync(ctx->cursor.p, 8, d_off, (size_t)8 << kFineShift, 8, groups, cudaMemcpyDeviceToDevice,
-                       ctx->stream));
-  CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));  // level-1 output (reuses exchange buffers)
+  CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));  // scratch (reuses the exchange buffers)
   CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
-  ScatterArgs s{};
-  s.desc_in = ctx->desc_pre.as<uint64_t>();
-  s.bin_in = ctx->bin_pre.as<uint32_t>();
-  s.n = n_sm;
-  s.n_bins = B;
-  s.bin_shift = kFineShift;
-  s.cursor = ctx->cursor.as<unsigned long long>();
-  s.desc_out = ctx->send_desc.as<uint64_t>();
-  // descriptors below 2^54 (positions < 2^43 bases) carry the fine bin in their top bits:
-  // the first level then stores 8 bytes per super-mer instead of 8 + 4 at two addresses
-  const bool pack = n_bases < (1ull << 43);
-  if (pack) s.pack_low_bits = kFineShift;
-  else s.bin_out = ctx->send_bin.as<uint32_t>();
+  CK(ctx->p_tmp.ensure(group_shuffle_scratch_bytes(B)));
+  GroupShuffleArgs gs{};
+  gs.desc_in = ctx->desc_pre.as<uint64_t>();
+  gs.bin_in = ctx->bin_pre.as<uint32_t>();
+  gs.n = n_sm;
+  gs.n_bins = B;
+  gs.tmp_desc = ctx->send_desc.as<uint64_t>();
+  gs.tmp_bin = ctx->send_bin.as<uint32_t>();
+  gs.desc_alt = ctx->desc_pre.as<uint64_t>();
+  gs.desc_out = ctx->desc_sorted.as<uint64_t>();
+  gs.off = d_off;
+  gs.win = d_win;
+  gs.scratch = ctx->p_tmp.as<unsigned long long>();
   {
-    Timer tm(ctx, K_SHUFFLE, nullptr, true, 2);
-    CK(launch_scatter(s, ctx->sms, ctx->stream));
-    if (pack)
-      CK(launch_regroup_fine_packed(ctx->send_desc.as<uint64_t>(), d_off, B, kFineShift,
-                                    ctx->desc_sorted.as<uint64_t>(), ctx->stream));
-    else
-      CK(launch_regroup_fine(ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), d_off, B, kFineShift,
-                             ctx->desc_sorted.as<uint64_t>(), ctx->stream));
+    const uint32_t G = group_shuffle_groups(B);
+    Timer tm(ctx, K_SHUFFLE, nullptr, true, G > 64 ? 5 : 4);
+    CK(launch_group_shuffle(gs, ctx->sms, ctx->stream));
   }
   trace("scatter issued");
   const uint32_t max_fill = smem_max_fill(cap);
@@ -1149,7 +1137,7 @@ gerbil_status build_dfp_table(gerbil_ctx* ctx, const SupermerArgs& a, uint64_t n
 // ---------------------------------------------------------------------------
 gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
                            const uint64_t* rstart, uint64_t n_reads, uint64_t n_bases, uint32_t k,
-                           uint32_t m, uint32_t B, bool want_mu, uint64_t& n_sm) {
+                           uint32_t m, uint32_t B, bool want_mu, uint64_t& n_sm, bool want_hist = true) {
   const uint32_t w = k - m + 1;
   uint64_t cap = (uint64_t)((double)n_bases * 2.0 / (w + 1) * 1.3) + (n_bases / kTile + 1) * 4 + 1024;
   Counters* dc = ctx->counters.as<Counters>();
@@ -1158,7 +1146,7 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     CK(ctx->bin_pre.ensure(cap * 4));
     if (want_mu) CK(ctx->mu_dbg.ensure(cap * 4));
     CK(cudaMemsetAsync(dc, 0, sizeof(Counters), ctx->stream));
-    CK(cudaMemsetAsync(ctx->hist.p, 0, 3ull * B * 8, ctx->stream));
+    if (want_hist) CK(cudaMemsetAsync(ctx->hist.p, 0, 3ull * B * 8, ctx->stream));
     SupermerArgs a{};
     a.codes = codes;
     a.nmask = nmask;
@@ -1176,9 +1164,9 @@ gerbil_status run_supermer(gerbil_ctx* ctx, const uint64_t* codes, const uint64_
     a.n_supermers = &dc->n_supermers;
     a.n_windows = &dc->n_windows;
     unsigned long long* h = ctx->hist.as<unsigned long long>();
-    a.bin_windows = h;
-    a.bin_supermers = h + B;
-    a.bin_words = (ctx->comm || ctx->want_words) ? h + 2 * B : nullptr;
+    a.bin_windows = want_hist ? h : nullptr;
+    a.bin_supermers = want_hist ? h + B : nullptr;
+    a.bin_words = (want_hist && (ctx->comm || ctx->want_words)) ? h + 2 * B : nullptr;
     const UploadPlan* up = ctx->upload;
     a.order_rank = nullptr;
     if (ctx->cfg.ordering == GERBIL_ORDER_DFP) {
@@ -1276,16 +1264,21 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   ctx->stats.input_bases = n_bases;
   ctx->stats.input_reads = n_reads;
 
+  // the device-planned path (single rank, many bins) groups super-mers with the group-major
+  // shuffle, which derives the bin histogram itself: step (b) then skips it
+  const uint32_t smem_cap = (!ctx->comm && !ctx->rec_out && B >= kDevicePlanBins && B <= (1u << 22) &&
+                             n_bases < (1ull << 43))
+                                ? smem_slots_for(ctx, k)
+                                : 0u;
   // (b)
   uint64_t n_sm = 0;
   trace("supermer issue");
-  CKS(run_supermer(ctx, codes, nmask, rstart, n_reads, n_bases, k, m, B, false, n_sm));
+  CKS(run_supermer(ctx, codes, nmask, rstart, n_reads, n_bases, k, m, B, false, n_sm, smem_cap == 0));
   trace("supermer done (synced)");
   const uint64_t local_windows = ctx->h_counters->n_windows;
   ctx->stats.supermers = n_sm;
   ctx->stats.valid_windows = local_windows;
   uint64_t owned_windows = 0;
-  const uint32_t smem_cap = (!ctx->comm && !ctx->rec_out && B >= kDevicePlanBins) ? smem_slots_for(ctx, k) : 0u;
   if (smem_cap) {
     // many bins, one rank: steps (c)-(e) planned on the device (no per-bin host work)
     CKS(count_local_device_plan(ctx, codes, n_sm, B, smem_cap, k, min_count, local_windows, n_bases));

@@ -14,17 +14,22 @@
 //    while the current chunk is counted — across bin boundaries too;
 //  - lanes take consecutive windows (32 per round), extract from the stage,
 //    canonicalise c = min(x, rc x) and hash;
-//  - insertion is warp-synchronous on the warp's private table: every pending
-//    lane probes linearly (plain shared loads) until it sees its key or an
-//    empty slot; lanes that stopped at the same slot form one group
-//    (__match_any_sync); the group's leader adds the group's size to the
-//    found count, or writes its key with the number of lanes that carry the
-//    same key into the empty slot — the others of that group probe on. No
-//    atomics, no locks: one writer per slot per step, __syncwarp between;
-//  - when the bin is done its table is compacted in place: counts >=
+//  - insertion into the warp's private table ("lock entries
+//    with atomics", here shared-memory atomics of one warp): every pending lane
+//    probes linearly (plain shared loads) until it sees its key or an empty
+//    slot; after a __syncwarp (all probes of the step done before any write) a
+//    lane that found its key adds 1 to the count (atomicAdd) and is done; a
+//    lane at an empty slot claims it with atomicCAS(count: 0 → 1) and, if it
+//    won, writes its key and appends the slot to the warp's list of occupied
+//    slots; losers re-probe from that slot in the next step (after a
+//    __syncwarp the winner's key is complete), where a same-key loser finds
+//    it. A key lives in at most one slot: a slot is claimed once and probes
+//    see only complete keys;
+//  - when the bin is done its occupied-slot list is compacted: counts >=
 //    min_count are written as (W key words, u32 count) at a range reserved
 //    with one global atomic per bin (reading Q5), Σcount and
-//    distinct are accumulated, and the slots are cleared for the next bin.
+//    distinct are accumulated, and the listed slots are cleared for the next
+//    bin (the scan touches the bin's distinct k-mers, not its table).
 //
 // A bin whose distinct k-mers exceed max_fill (a skewed bin the host's ρ̂
 // estimate did not predict) is abandoned without output and its list index
@@ -102,6 +107,20 @@ struct SmemTable {
     if (PACK) slots()[s] = make_ulonglong2(0ull, 0ull);
     else counts()[s] = 0u;
   }
+  __device__ __forceinline__ uint32_t* count_ptr(uint32_t s) const {
+    return PACK ? reinterpret_cast<uint32_t*>(slots() + s) + 2 : counts() + s;  // low half of .y
+  }
+  // the key of a slot this lane just claimed (its count is already set)
+  __device__ __forceinline__ void put_key(uint32_t s, const uint64_t (&c)[W]) const {
+    if (PACK) {
+      uint64_t* q = reinterpret_cast<uint64_t*>(slots() + s);
+      q[0] = c[0];
+      if (W == 2) reinterpret_cast<uint32_t*>(q)[3] = (uint32_t)(c[W - 1] >> 32);  // high half of .y
+    } else {
+#pragma unroll
+      for (int v = 0; v < W; ++v) keys()[(size_t)s * W + v] = c[v];
+    }
+  }
 };
 
 // k-mer of k bases at base offset o of a staged stream (S words), W left-aligned words
@@ -165,7 +184,7 @@ __host__ __device__ constexpr uint32_t smem_overhead(int S) {
 }
 
 // Per-warp shared memory: [fwd stage 2][32][S] u64 | [rc stage][32][S] u64 | map u8[1024] |
-// table (cap slots) | tags u8[cap]
+// table (cap slots) | occupied-slot list u16[cap]
 template <int W, bool PACK>
 __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemCountArgs a, uint32_t warp_bytes) {
   constexpr int S = smem_stage_words(PACK);
@@ -179,7 +198,7 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
   const uint32_t tail = 2 * a.k - 64 * (W - 1);  // meaningful bits of the last key word
   const uint64_t tmask = tail < 64 ? ~0ull << (64 - tail) : ~0ull;
   SmemTable<W, PACK> T{map + kMapWindows, cap};
-  uint8_t* tags = map + kMapWindows + (size_t)cap * (PACK ? 16u : 8u * W + 4u);
+  uint16_t* occ = reinterpret_cast<uint16_t*>(map + kMapWindows + (size_t)cap * (PACK ? 16u : 8u * W + 4u));
   for (uint32_t s = lane; s < cap; s += 32) T.clear(s);
   __syncwarp();
 
@@ -330,95 +349,67 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
         }
         uint32_t h = (uint32_t)(((uint64_t)smem_hash<W>(c) * cb) >> 32);
 
-        // warp-synchronous insertion into the warp's private table. A table never fills
+        // insertion into the warp's private table (header). A table never fills
         // (abandonment at max_fill <= cap - 32, or windows < slots), so probing ends.
         bool pend = act;
         for (;;) {
-          uint32_t st = 0, oc = 0;  // st: 1 = found (count oc), 2 = empty slot
+          bool found = false;
           if (pend) {
             for (;;) {
               bool eq;
               const uint32_t cnt = T.probe(h, c, eq);
-              if (cnt == 0u) {
-                st = 2;
-                break;
-              }
+              if (cnt == 0u) break;
               if (eq) {
-                st = 1;
-                oc = cnt;
+                found = true;
                 break;
               }
               h = (h + 1 == cb) ? 0u : h + 1;
             }
-            tags[h] = (uint8_t)lane;  // fast path: one lane per target slot (write, read back)
           }
-          __syncwarp();
-          const bool win = pend && tags[h] == (uint8_t)lane;
-          const uint32_t clash = __ballot_sync(kFull, pend && !win) | (a.dbg & 4u);
-          if (clash == 0u) {
-            if (win) {
-              if (st == 1u) T.set_count(h, oc + 1u);
-              else T.put(h, c, 1u);
+          __syncwarp();  // every probe of this step before any write
+          bool won = false;
+          if (pend) {
+            if (found) {
+              atomicAdd(T.count_ptr(h), 1u);
+              pend = false;
+            } else if (atomicCAS(T.count_ptr(h), 0u, 1u) == 0u) {
+              T.put_key(h, c);
+              won = true;
+              pend = false;
             }
-            n_distinct += __popc(__ballot_sync(kFull, win && st == 2u));
-            __syncwarp();
-            break;
           }
-          // several lanes on one slot: group them (__match_any_sync); the leader adds the
-          // group's size to a found count, or writes its key with the number of lanes
-          // carrying the same key into the empty slot — the others probe on
-          const uint32_t grp = __match_any_sync(kFull, pend ? h : kFull);
-          const uint32_t leader = __ffs(grp) - 1;
-          bool same = st == 1u;  // a found slot holds exactly this key for every lane of the group
-          {
-            bool e = true;
-#pragma unroll
-            for (int v = 0; v < W; ++v) {  // every lane shuffles every word (no short-circuit)
-              const uint64_t lv = __shfl_sync(kFull, c[v], leader);
-              e = e && lv == c[v];
-            }
-            if (st == 2u) same = e;
-          }
-          const uint32_t sm = __ballot_sync(kFull, same) & grp;
-          const bool lead = pend && lane == leader;
-          if (lead) {
-            if (st == 1u) T.set_count(h, oc + __popc(sm));
-            else T.put(h, c, __popc(sm));
-          }
-          n_distinct += __popc(__ballot_sync(kFull, lead && st == 2u));
-          if (same) pend = false;
-          __syncwarp();
-          if (!__any_sync(kFull, pend)) break;
+          const uint32_t wm = __ballot_sync(kFull, won);
+          if (won) occ[n_distinct + __popc(wm & ((1u << lane) - 1u))] = (uint16_t)h;
+          n_distinct += __popc(wm);
+          const bool more = __any_sync(kFull, pend);
+          __syncwarp();  // claimed keys complete before anyone probes again
+          if (!more) break;
         }
         if (n_distinct > fill) abandoned = true;
         if (abandoned) break;
       }
     }
 
-    if (f0 & 2u) {  // last chunk of the bin: output or abandon, clear the table
+    if (f0 & 2u) {  // last chunk of the bin: output or abandon; clear the occupied slots
+      __syncwarp();
       if (!abandoned) {
         uint32_t keep = n_distinct;  // min_count 1: every occupied slot is output
         if (a.min_count > 1) {
           keep = 0;
-          for (uint32_t s = lane; s < cb; s += 32) {
-            const uint32_t n = T.count(s);
-            keep += n >= a.min_count ? 1u : 0u;
-          }
+          for (uint32_t i = lane; i < n_distinct; i += 32) keep += T.count(occ[i]) >= a.min_count ? 1u : 0u;
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) keep += __shfl_xor_sync(kFull, keep, off);
         }
         unsigned long long off = 0;
         if (lane == 0 && keep) off = atomicAdd(a.out_n, (unsigned long long)keep);
         off = __shfl_sync(kFull, off, 0);
-        for (uint32_t s0 = 0; s0 < cb; s0 += 32) {
-          const uint32_t s = s0 + lane;
-          const uint32_t n = T.count(s);
+        for (uint32_t i0 = 0; i0 < n_distinct; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          const uint32_t s = i < n_distinct ? occ[i] : 0u;
+          const uint32_t n = i < n_distinct ? T.count(s) : 0u;
           const bool kp = n >= a.min_count && n != 0u;
           const uint32_t km = __ballot_sync(kFull, kp);
-          if (n) {
-            acc_sum += n;
-            acc_dist += 1;
-          }
+          acc_sum += n;
           if (kp) {
             const unsigned long long oi = off + __popc(km & ((1u << lane) - 1u));
             if (oi < a.out_cap) {
@@ -430,10 +421,11 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
             }
           }
           off += __popc(km);
-          T.clear(s);
+          if (i < n_distinct) T.clear(s);
         }
+        acc_dist += lane == 0 ? n_distinct : 0u;
       } else {
-        for (uint32_t s = lane; s < cb; s += 32) T.clear(s);
+        for (uint32_t i = lane; i < n_distinct; i += 32) T.clear(occ[i]);
         if (lane == 0) {
           const unsigned long long e = atomicAdd(a.n_failed, 1ull);
           a.failed[2 * e] = a.range[2 * (size_t)l0];  // the bin's range entry, for the L2 recount
@@ -508,7 +500,7 @@ int smem_count_warps(uint32_t k) {
   return v < 1 ? 1 : (v > kSmemMaxWarps ? kSmemMaxWarps : v);
 }
 
-uint32_t smem_slot_bytes(uint32_t k) { return (smem_pack(k) ? 16u : 8u * key_words(k) + 4u) + 1u /* tag */; }
+uint32_t smem_slot_bytes(uint32_t k) { return (smem_pack(k) ? 16u : 8u * key_words(k) + 4u) + 2u /* list */; }
 
 uint32_t smem_warp_bytes(uint32_t k, uint32_t cap) {
   return (smem_overhead(smem_stage_words(smem_pack(k))) + cap * smem_slot_bytes(k) + 15u) & ~15u;

@@ -103,6 +103,26 @@ cudaError_t launch_regroup_fine(const uint64_t* desc_in, const uint32_t* bin_in,
 cudaError_t launch_regroup_fine_packed(const uint64_t* desc_in, const unsigned long long* off, uint32_t n_bins,
                                        uint32_t shift, uint64_t* desc_out, cudaStream_t s);
 
+// Group-major shuffle (shuffle.cu, single rank, n_bins <= 2^22, descriptors < 2^54): groups the
+// step-(b) output by bin without any per-super-mer global atomic and derives every bin's offset
+// and windows on the way (no step-(b) histogram needed). desc_alt may alias desc_in.
+struct GroupShuffleArgs {
+  const uint64_t* desc_in;      // [n] step (b) descriptors
+  const uint32_t* bin_in;       // [n] their bins
+  uint64_t n;
+  uint32_t n_bins;
+  uint64_t* tmp_desc;           // [n] scratch
+  uint32_t* tmp_bin;            // [n] scratch
+  uint64_t* desc_alt;           // [n] scratch (may be desc_in)
+  uint64_t* desc_out;           // [n] bin-ordered descriptors
+  unsigned long long* off;      // [n_bins + 1] first descriptor of each bin (out)
+  unsigned long long* win;      // [n_bins] windows per bin (out)
+  unsigned long long* scratch;  // group_shuffle_scratch_bytes(n_bins)
+};
+uint32_t group_shuffle_groups(uint32_t n_bins);
+size_t group_shuffle_scratch_bytes(uint32_t n_bins);
+cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_t s);
+
 // world > 1: copy every local super-mer (descriptor + word-aligned payload)
 // into the send buffer, ordered by (destination rank, bin).
 struct PackArgs {
@@ -163,7 +183,7 @@ struct SmemCountArgs {
   unsigned long long* distinct;
   unsigned long long* failed;        // [n_list][2] range entries of abandoned bins
   unsigned long long* n_failed;
-  uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 4 = no tag fast path
+  uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 8 = full-size tables
   int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match
 };
 // Table slots a bin of `win` windows gets (count_smem_kernel): windows * 1.25 + 32, rounded up to 32,

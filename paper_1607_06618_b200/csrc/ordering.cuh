@@ -50,9 +50,9 @@ __device__ __forceinline__ uint32_t order_key(uint32_t v, const OrderCtx& o) {
   const uint32_t lo = v & 0x55555555u, hi = (v >> 1) & 0x55555555u, dig = o.mask & 0x55555555u;
   switch (ORD == kOrdRuntime ? o.ordering : ORD) {
     case kOrdKMC2:
-      if (o.m >= 3) {
+      if (o.m >= 3) {  // prefix AAA (000000) or ACA (000100): demoted
         const uint32_t pre = v >> (2 * o.m - 6);
-        if (pre == 0u || pre == 4u) return v | (1u << (2 * o.m));
+        return v | ((uint32_t)((pre & ~4u) == 0u) << (2 * o.m));
       }
       return v;
     case kOrdCGAT:

@@ -150,7 +150,340 @@ __global__ void __launch_bounds__(kFineThreads) regroup_fine_packed_kernel(const
   }
 }
 
+// ---- group-major bin shuffle (single rank, many bins) -------------------------------
+// Super-mers are grouped by bin in three passes, none with a per-super-mer global atomic:
+//   0. group histogram: counts per group g = bin >> 10 (<= 4096 groups), one shared-memory
+//      histogram per CTA;
+//   A. partition by the group's high digit g >> 6 (64 buckets), B. partition every
+//      high-digit segment by the low digit g & 63 (64 buckets): a chunk ranks its elements
+//      per bucket with warp-aggregated shared-memory counters, reserves one global range per
+//      (chunk, bucket), stages the chunk bucket-major in shared memory and writes runs
+//      (coalesced). Pass B stores 8 bytes: the fine bin (bin & 1023) rides in descriptor
+//      bits 54.. (kDescPackShift);
+//   C. per group: counts and windows of its 1024 fine bins (shared memory), their offsets and
+//      windows to global memory (the bin plan's inputs), then the fine scatter.
+
+constexpr int kGroupShift = 10;   // fine bins per group = 1024
+constexpr int kDigits = 64;       // buckets per partition pass
+constexpr int kPartThreads = 256;
+constexpr int kPartPer = 16;
+constexpr int kPartChunk = kPartThreads * kPartPer;
+
+__global__ void __launch_bounds__(256) group_hist_kernel(const uint32_t* __restrict__ bin, uint64_t n, uint32_t G,
+                                                         unsigned long long* __restrict__ cnt) {
+  extern __shared__ uint32_t s_h[];
+  for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) s_h[g] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&s_h[__ldg(bin + i) >> kGroupShift], 1u);
+  __syncthreads();
+  for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
+    if (s_h[g]) atomicAdd(&cnt[g], (unsigned long long)s_h[g]);
+}
+
+// One CTA: group offsets (exclusive scan of cnt[G], padded with the total up to
+// 64 * n_seg + 1 entries), pass-A cursors (the high digits' first groups), pass-B cursors
+// (every group's start), pass-B segment bounds and first chunk per segment.
+__global__ void __launch_bounds__(1024) part_setup_kernel(const unsigned long long* __restrict__ cnt, uint32_t G,
+                                                          uint32_t n_seg, unsigned long long* goff,
+                                                          unsigned long long* cur_a, unsigned long long* cur_b,
+                                                          unsigned long long* seg_b, unsigned long long* chunk_b,
+                                                          uint64_t n, unsigned long long* seg_a,
+                                                          unsigned long long* chunk_a) {
+  __shared__ unsigned long long s_w[32];
+  if (threadIdx.x == 0) {  // pass A: one segment [0, n)
+    seg_a[0] = 0ull;
+    seg_a[1] = n;
+    chunk_a[0] = 0ull;
+    chunk_a[1] = (n + kPartChunk - 1) / kPartChunk;
+  }
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t padded = n_seg * kDigits;  // >= G
+  const uint32_t per = (padded + 1023) / 1024;
+  unsigned long long v[8];  // padded <= 4096 + 63 → per <= 5
+  unsigned long long s = 0;
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t g = tid * per + j;
+    v[j] = g < G ? cnt[g] : 0ull;
+    s += v[j];
+  }
+  unsigned long long incl = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long x = s_w[lane], y = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= (uint32_t)o) y += t;
+    }
+    s_w[lane] = y - x;
+  }
+  __syncthreads();
+  unsigned long long run = s_w[warp] + incl - s;
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t g = tid * per + j;
+    if (g < padded) {
+      goff[g] = run;
+      if (g < G) cur_b[g] = run;
+      if ((g & (kDigits - 1)) == 0) {
+        cur_a[g / kDigits] = run;
+        seg_b[g / kDigits] = run;
+      }
+    }
+    run += v[j];
+  }
+  if (tid == 1023) {
+    goff[padded] = run;  // run = total
+    seg_b[n_seg] = run;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long c = 0;
+    for (uint32_t q = 0; q < n_seg; ++q) {
+      chunk_b[q] = c;
+      const unsigned long long len = seg_b[q + 1] - seg_b[q];
+      c += (len + kPartChunk - 1) / kPartChunk;
+    }
+    chunk_b[n_seg] = c;
+  }
+}
+
+// One partition pass (A: n_seg == 1 over [0, n); B: n_seg segments from seg[], chunks
+// numbered per chunk_first[]). digit = (bin >> shift) & 63; cursors cur[seg * 64 + digit].
+template <bool PACK_OUT>
+__global__ void __launch_bounds__(kPartThreads) partition64_kernel(
+    const uint64_t* __restrict__ desc_in, const uint32_t* __restrict__ bin_in, uint32_t n_seg,
+    const unsigned long long* __restrict__ seg, const unsigned long long* __restrict__ chunk_first, uint32_t shift,
+    unsigned long long* cur, uint64_t* __restrict__ desc_out, uint32_t* __restrict__ bin_out) {
+  extern __shared__ uint64_t s_desc[];  // [kPartChunk], then u32 bins [kPartChunk]
+  uint32_t* s_bin = reinterpret_cast<uint32_t*>(s_desc + kPartChunk);
+  __shared__ uint32_t s_cnt[kDigits], s_loc[kDigits];
+  __shared__ unsigned long long s_gb[kDigits];
+  __shared__ unsigned long long s_chunk[65];
+  const uint32_t tid = threadIdx.x, lane = lane_id();
+  for (uint32_t q = tid; q <= n_seg; q += blockDim.x) s_chunk[q] = chunk_first[q];
+  __syncthreads();
+  const unsigned long long n_chunks = s_chunk[n_seg];
+  for (unsigned long long c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    uint32_t sg = 0;  // segment of chunk c: last q with s_chunk[q] <= c
+    for (uint32_t step = 32; step >= 1; step >>= 1)
+      if (sg + step <= n_seg - 1 && s_chunk[sg + step] <= c) sg += step;
+    const unsigned long long e = seg[sg + 1];
+    const unsigned long long i0 = seg[sg] + (c - s_chunk[sg]) * kPartChunk;
+    if (tid < kDigits) s_cnt[tid] = 0;
+    __syncthreads();
+    uint64_t d[kPartPer];
+    uint32_t b[kPartPer], rk[kPartPer];
+#pragma unroll
+    for (int j = 0; j < kPartPer; ++j) {
+      const unsigned long long i = i0 + j * kPartThreads + tid;
+      const bool act = i < e;
+      d[j] = act ? __ldg(desc_in + i) : 0ull;
+      b[j] = act ? __ldg(bin_in + i) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < kPartPer; ++j) {
+      const bool act = b[j] != 0xffffffffu;
+      const uint32_t dg = act ? (b[j] >> shift) & (kDigits - 1) : kDigits + lane;  // inactive lanes stay alone
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      const uint32_t leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (act && lane == leader) base = atomicAdd(&s_cnt[dg], (uint32_t)__popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      rk[j] = base + __popc(peers & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    if (tid < 32) {  // local exclusive offsets of the 64 buckets, global ranges
+      const uint32_t x0 = s_cnt[2 * tid], x1 = s_cnt[2 * tid + 1];
+      uint32_t incl = x0 + x1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      const uint32_t ex = incl - x0 - x1;
+      s_loc[2 * tid] = ex;
+      s_loc[2 * tid + 1] = ex + x0;
+      if (x0) s_gb[2 * tid] = atomicAdd(&cur[sg * kDigits + 2 * tid], (unsigned long long)x0);
+      if (x1) s_gb[2 * tid + 1] = atomicAdd(&cur[sg * kDigits + 2 * tid + 1], (unsigned long long)x1);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPartPer; ++j) {
+      if (b[j] == 0xffffffffu) continue;
+      const uint32_t p = s_loc[(b[j] >> shift) & (kDigits - 1)] + rk[j];
+      s_desc[p] = d[j];
+      s_bin[p] = b[j];
+    }
+    __syncthreads();
+    const uint32_t tot = e - i0 < (unsigned long long)kPartChunk ? (uint32_t)(e - i0) : (uint32_t)kPartChunk;
+    for (uint32_t p = tid; p < tot; p += kPartThreads) {
+      const uint32_t bb = s_bin[p];
+      const uint32_t dg = (bb >> shift) & (kDigits - 1);
+      const unsigned long long o = s_gb[dg] + (p - s_loc[dg]);
+      if (PACK_OUT) {
+        desc_out[o] = s_desc[p] | ((uint64_t)(bb & ((1u << kGroupShift) - 1u)) << kDescPackShift);
+      } else {
+        desc_out[o] = s_desc[p];
+        bin_out[o] = bb;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Pass C: one CTA per group. Fine-bin counts and windows, the bins' offsets/windows out,
+// then the scatter into bin order (descriptor bits 54.. cleared).
+constexpr int kFineT = 512;
+constexpr int kFineU = 8;
+__global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t* __restrict__ desc_in,
+                                                                 const unsigned long long* __restrict__ goff,
+                                                                 uint32_t n_bins, unsigned long long* __restrict__ off,
+                                                                 unsigned long long* __restrict__ win,
+                                                                 uint64_t* __restrict__ desc_out) {
+  constexpr uint32_t kFan = 1u << kGroupShift;
+  __shared__ uint32_t s_cur[kFan];
+  __shared__ unsigned long long s_win[kFan];
+  __shared__ uint32_t s_w[kFineT / 32];
+  const uint32_t g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t b0 = g << kGroupShift;
+  const unsigned long long i0 = goff[g], i1 = goff[g + 1];
+  for (uint32_t t = tid; t < kFan; t += kFineT) {
+    s_cur[t] = 0;
+    s_win[t] = 0;
+  }
+  __syncthreads();
+  constexpr uint64_t kLow = (1ull << kDescPackShift) - 1;
+  for (unsigned long long base = i0; base < i1; base += (unsigned long long)kFineT * kFineU) {
+    uint64_t d[kFineU];
+#pragma unroll
+    for (int u = 0; u < kFineU; ++u) {
+      const unsigned long long i = base + u * kFineT + tid;
+      d[u] = i < i1 ? __ldg(desc_in + i) : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kFineU; ++u)
+      if (d[u] != ~0ull) {
+        const uint32_t f = (uint32_t)(d[u] >> kDescPackShift);
+        atomicAdd(&s_cur[f], 1u);
+        atomicAdd(&s_win[f], (unsigned long long)((d[u] & ((1u << kNwinBits) - 1)) + 1));
+      }
+  }
+  __syncthreads();
+  // exclusive scan of the 1024 counts: 2 per thread
+  const uint32_t x0 = s_cur[2 * tid], x1 = s_cur[2 * tid + 1];
+  uint32_t incl = x0 + x1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += t;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < kFineT / 32 ? s_w[lane] : 0u;
+    uint32_t y = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= (uint32_t)o) y += t;
+    }
+    if (lane < kFineT / 32) s_w[lane] = y - x;
+  }
+  __syncthreads();
+  const uint32_t ex = s_w[warp] + incl - x0 - x1;
+  s_cur[2 * tid] = ex;
+  s_cur[2 * tid + 1] = ex + x0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t b = b0 + 2 * tid + q;
+    if (b < n_bins) {
+      off[b] = i0 + (q ? ex + x0 : ex);
+      win[b] = s_win[2 * tid + q];
+    }
+  }
+  if (b0 + kFan >= n_bins && tid == 0) off[n_bins] = i1;  // the last group closes the offsets
+  __syncthreads();
+  for (unsigned long long base = i0; base < i1; base += (unsigned long long)kFineT * kFineU) {
+    uint64_t d[kFineU];
+    uint32_t p[kFineU];
+#pragma unroll
+    for (int u = 0; u < kFineU; ++u) {
+      const unsigned long long i = base + u * kFineT + tid;
+      d[u] = i < i1 ? __ldg(desc_in + i) : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kFineU; ++u)
+      if (d[u] != ~0ull) p[u] = atomicAdd(&s_cur[(uint32_t)(d[u] >> kDescPackShift)], 1u);
+#pragma unroll
+    for (int u = 0; u < kFineU; ++u)
+      if (d[u] != ~0ull) desc_out[i0 + p[u]] = d[u] & kLow;
+  }
+}
+
 }  // namespace
+
+uint32_t group_shuffle_groups(uint32_t n_bins) { return ((n_bins - 1) >> kGroupShift) + 1; }
+
+cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_t st) {
+  const uint32_t G = group_shuffle_groups(a.n_bins);
+  if (G > kDigits * kDigits) return cudaErrorInvalidValue;
+  const uint32_t n_seg = (G + kDigits - 1) / kDigits;
+  unsigned long long* cnt = a.scratch;                    // [G]
+  unsigned long long* goff = cnt + G;                     // [64 n_seg + 1]
+  unsigned long long* cur_a = goff + n_seg * kDigits + 1; // [64]
+  unsigned long long* cur_b = cur_a + kDigits;            // [G]
+  unsigned long long* seg_a = cur_b + G;                  // [2]
+  unsigned long long* chunk_a = seg_a + 2;                // [2]
+  unsigned long long* seg_b = chunk_a + 2;                // [n_seg + 1]
+  unsigned long long* chunk_b = seg_b + n_seg + 1;        // [n_seg + 1]
+  cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)G * 8, st);
+  if (e != cudaSuccess) return e;
+  if (a.n == 0) {
+    e = cudaMemsetAsync(a.off, 0, ((size_t)a.n_bins + 1) * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.win, 0, (size_t)a.n_bins * 8, st);
+    return e;
+  }
+  {
+    const size_t dyn = (size_t)G * 4;
+    e = cudaFuncSetAttribute(group_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    uint64_t grid = (a.n + 255) / 256;
+    if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+    group_hist_kernel<<<(unsigned)grid, 256, dyn, st>>>(a.bin_in, a.n, G, cnt);
+  }
+  part_setup_kernel<<<1, 1024, 0, st>>>(cnt, G, n_seg, goff, cur_a, cur_b, seg_b, chunk_b, a.n, seg_a, chunk_a);
+  constexpr size_t kPartSmem = (size_t)kPartChunk * 12;
+  for (auto kern : {partition64_kernel<false>, partition64_kernel<true>}) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem);
+    if (e != cudaSuccess) return e;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, partition64_kernel<true>, kPartThreads, kPartSmem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t max_chunks = (a.n + kPartChunk - 1) / kPartChunk + n_seg;
+  uint64_t grid = (uint64_t)sms * per_sm;
+  if (grid > max_chunks) grid = max_chunks;
+  const uint64_t* pb_desc = a.desc_in;
+  const uint32_t* pb_bin = a.bin_in;
+  if (n_seg > 1) {  // pass A by the high digit
+    partition64_kernel<false><<<(unsigned)grid, kPartThreads, kPartSmem, st>>>(
+        a.desc_in, a.bin_in, 1, seg_a, chunk_a, kGroupShift + 6, cur_a, a.tmp_desc, a.tmp_bin);
+    pb_desc = a.tmp_desc;
+    pb_bin = a.tmp_bin;
+  }
+  uint64_t* packed = n_seg > 1 ? a.desc_alt : a.tmp_desc;  // pass B output: never its own input
+  partition64_kernel<true><<<(unsigned)grid, kPartThreads, kPartSmem, st>>>(pb_desc, pb_bin, n_seg, seg_b, chunk_b,
+                                                                   kGroupShift, cur_b, packed, nullptr);
+  regroup_counted_kernel<<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);
+  return cudaGetLastError();
+}
+
+size_t group_shuffle_scratch_bytes(uint32_t n_bins) {
+  const uint32_t G = group_shuffle_groups(n_bins), n_seg = (G + kDigits - 1) / kDigits;
+  return ((size_t)G * 2 + n_seg * kDigits + 1 + kDigits + 4 + 2 * ((size_t)n_seg + 1)) * 8;
+}
 
 cudaError_t launch_regroup_fine_packed(const uint64_t* desc_in, const unsigned long long* off, uint32_t n_bins,
                                        uint32_t shift, uint64_t* desc_out, cudaStream_t st) {

@@ -253,12 +253,25 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
       const uint32_t q = s0 + k - 1, qs = q & 31;
       uint32_t n8 = s_n[q >> 5] >> qs;
       if (qs > 24) n8 |= s_n[(q >> 5) + 1] << (32 - qs);
+      if (k > kPer) {
+        // bit masks over the 8 windows: an X among the thread's own positions at or after
+        // s0+i lies closer than k-1 (< kPer <= k-2), so window i needs none (A); the next X
+        // from s0+8 on must be >= s0+i+k-1 (B); base s0+i+k-1 not N (~n8); window in range (D)
+        const uint32_t A = x8 ? (0xffu & ~((2u << (31 - __clz(x8))) - 1u)) : 0xffu;
+        const int t = (int)ns2 - (int)(s0 + k - 1);  // windows i <= t pass B
+        const uint32_t B = t >= kPer - 1 ? 0xffu : (t < 0 ? 0u : (2u << t) - 1u);
+        const uint64_t base = p0 + s0;
+        const uint32_t D = base >= end_p ? 0u : (end_p - base >= (uint64_t)kPer ? 0xffu
+                                                                             : (1u << (uint32_t)(end_p - base)) - 1u);
+        vmask = A & B & ~n8 & D & 0xffu;
+      } else {
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        const uint32_t xi = x8 >> i;
-        const uint32_t nxt = xi ? s0 + i + __ffs(xi) - 1 : ns2;
-        const bool valid = p0 + s0 + i < end_p && nxt >= s0 + i + k - 1 && !((n8 >> i) & 1u);
-        vmask |= (uint32_t)valid << i;
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t xi = x8 >> i;
+          const uint32_t nxt = xi ? s0 + i + __ffs(xi) - 1 : ns2;
+          const bool valid = p0 + s0 + i < end_p && nxt >= s0 + i + k - 1 && !((n8 >> i) & 1u);
+          vmask |= (uint32_t)valid << i;
+        }
       }
       s_last[tid] = (vmask >> (kPer - 1)) & 1u ? mu[kPer - 1] : 0xffffffffu;
     }
@@ -327,7 +340,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
         atomicAdd(&h_win[b], nwin);
         atomicAdd(&h_cnt[b], 1u);
         if (a.bin_words) atomicAdd(&h_wrd[b], (nwin + k - 1 + 31) / 32);
-      } else {
+      } else if (a.bin_windows) {  // null: the bin shuffle derives the histogram (launch_group_shuffle)
         atomicAdd(&a.bin_windows[b], (unsigned long long)nwin);
         atomicAdd(&a.bin_supermers[b], 1ull);
         if (a.bin_words) atomicAdd(&a.bin_words[b], (unsigned long long)((nwin + k - 1 + 31) / 32));
@@ -370,7 +383,7 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
   const int nh = a.bin_words ? 3 : 2;
   // per-CTA smem histograms only while small: a large one would cap occupancy,
   // and spread global REDs are cheap next to this kernel's arithmetic
-  const int hist_smem = a.n_bins <= 2048;
+  const int hist_smem = a.n_bins <= 2048 && a.bin_windows != nullptr;
   const size_t dyn = hist_smem ? (size_t)nh * a.n_bins * sizeof(uint32_t) : 0;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);

@@ -72,8 +72,10 @@ supermer_reads_kernel(SupermerArgs a, unsigned long long* work) {
         a.bin[idx] = b;
         if (a.mu) a.mu[idx] = key;
       }
-      atomicAdd(&a.bin_windows[b], (unsigned long long)nwin);
-      atomicAdd(&a.bin_supermers[b], 1ull);
+      if (a.bin_windows) {
+        atomicAdd(&a.bin_windows[b], (unsigned long long)nwin);
+        atomicAdd(&a.bin_supermers[b], 1ull);
+      }
       if (a.bin_words) atomicAdd(&a.bin_words[b], (unsigned long long)((nwin + k - 1 + 31) / 32));
     }
     nbuf = 0;
