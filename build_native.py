@@ -28,7 +28,7 @@ NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-rela
 EXTRA = os.environ.get("GERBIL_NVCC_EXTRA", "").split()
 NVFLAGS += EXTRA
 
-GERBIL_CU = ["parse.cu", "supermer.cu", "supermer_reads.cu", "ordering.cu", "shuffle.cu", "count.cu", "count_smem.cu", "compact.cu", "comm.cu",
+GERBIL_CU = ["parse.cu", "supermer.cu", "supermer_reads.cu", "ordering.cu", "shuffle.cu", "count.cu", "count_wide.cu", "count_smem.cu", "compact.cu", "comm.cu",
              "api.cu"]
 GERBIL_CPP = ["reader.cpp", "output.cpp"]
 
@@ -79,7 +79,7 @@ def build_gerbil(force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         list(ex.map(_run, jobs))
     _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB_GERBIL,
-          "-ldl", "-lpthread"])
+          "-ldl", "-lpthread", "-lz"])
     return LIB_GERBIL
 
 

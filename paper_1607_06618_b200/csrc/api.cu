@@ -315,7 +315,7 @@ int wave_lanes() {
 gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t min_count) {
   if (!ctx) return GERBIL_E_USAGE;
   if (ctx->poisoned) return fail(ctx, GERBIL_E_STATE, "context poisoned by an earlier CUDA/NCCL error");
-  if (k < 8 || k > 200) return fail(ctx, GERBIL_E_USAGE, "k must be in [8, 200]");
+  if (k < 8 || k > 479) return fail(ctx, GERBIL_E_USAGE, "k must be in [8, 479]");
   if (m == 0) m = std::min<uint32_t>(7, k - 1);
   if (m > 15 || m >= k) return fail(ctx, GERBIL_E_USAGE, "m must be in [1, min(k-1, 15)]");
   if (min_count < 1) return fail(ctx, GERBIL_E_USAGE, "min_count must be >= 1");
@@ -739,7 +739,7 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
 
 // Shared-memory table slots per warp for this k (0 = shared-memory path off).
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
-  if (ctx->cfg.count_mode == 1) return 0;
+  if (ctx->cfg.count_mode == 1 || key_words(k) > 7) return 0;  // shared-memory tables: W <= 7
   if (!ctx->smem_optin &&
       cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
     cudaGetLastError();
@@ -2144,8 +2144,7 @@ gerbil_status gerbil_pack_reads(const gerbil_reads* reads, int32_t threads, uint
   std::string e;
   bool ok = true;
   if (has_text) ok = pack_text(reads->text, reads->text_len, threads, pb, e, "<memory>");
-  else
-    for (uint32_t i = 0; ok && i < reads->n_paths; ++i) ok = pack_file(reads->paths[i], threads, pb, e);
+  else ok = pack_files(reads->paths, reads->n_paths, threads, pb, e);
   if (!ok) {
     if (err && err_len) {
       strncpy(err, e.c_str(), err_len - 1);
@@ -2175,8 +2174,7 @@ gerbil_status gerbil_count(gerbil_ctx* ctx, const gerbil_reads* reads, uint32_t 
   std::string e;
   bool ok = true;
   if (has_text) ok = pack_text(reads->text, reads->text_len, ctx->cfg.host_threads, pb, e, "<memory>");
-  else
-    for (uint32_t i = 0; ok && i < reads->n_paths; ++i) ok = pack_file(reads->paths[i], ctx->cfg.host_threads, pb, e);
+  else ok = pack_files(reads->paths, reads->n_paths, ctx->cfg.host_threads, pb, e);
   if (!ok) return fail(ctx, GERBIL_E_IO, e);
   if (pb.read_start.empty()) pb.read_start.push_back(0);
   const double t_reader = wall_ms() - t0;
@@ -2287,8 +2285,8 @@ gerbil_status gerbil_debug_supermers(gerbil_ctx* ctx, const uint64_t* codes, con
                                      uint64_t capacity, uint64_t* n_out) {
   // step (b) alone accepts the small k of the paper's Fig. 1 example (k=4, m=3)
   if (!ctx) return GERBIL_E_USAGE;
-  if (k < 2 || k > 200 || m < 1 || m >= k || m > 15)
-    return fail(ctx, GERBIL_E_USAGE, "debug_supermers: need 2 <= k <= 200, 1 <= m < k, m <= 15");
+  if (k < 2 || k > 479 || m < 1 || m >= k || m > 15)
+    return fail(ctx, GERBIL_E_USAGE, "debug_supermers: need 2 <= k <= 479, 1 <= m < k, m <= 15");
   if (!rstart || !n_out) return fail(ctx, GERBIL_E_USAGE, "null argument");
   CK(cudaSetDevice(ctx->device));
   // host buffers in, like gerbil_count_host_packed

@@ -9,7 +9,7 @@
 
 namespace gerbil {
 
-constexpr int kMaxW = 7;          // k <= 200 → W = ceil(k/32) <= 7
+constexpr int kMaxW = 15;         // k <= 479 → W = ceil(k/32) <= 15
 constexpr uint32_t kSlotsPerBucket = 4;  // table.cuh bucket layout
 constexpr uint32_t kReady = 0x80000000u;
 constexpr uint32_t kFpMask = 0x7fffffffu;

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(CompactArgs a) {
       if (keep[j]) {
         const uint64_t idx = s_base + s_cnt[j * kWarps + warp] + rank[j];
         if (idx < a.cap) {
-          uint64_t ch[8], key[kMaxW];
+          uint64_t ch[kMaxW + 1], key[kMaxW];
           ch[0] = c0[j];
           if (inl) {
             ch[1] = c1[j] & 0xffffffff00000000ull;

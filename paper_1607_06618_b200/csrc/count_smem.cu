@@ -137,7 +137,7 @@ __device__ __forceinline__ void extract_stage(const uint64_t* s, uint32_t o, uin
 }
 
 // Same without bounds checks, from 32-bit funnel shifts: words past the k-mer may be
-// read (they stay inside the warp's shared memory: rc stage, map and table follow the
+// read (they stay inside the warp's shared memory: rc stage and table follow the
 // stages) but only feed bits that the tail mask clears. The stream's 32-bit units in
 // order are hi(w0), lo(w0), hi(w1), ...; the k-mer starts in unit 2*(o/32) + (o%32)/16.
 template <int W>
@@ -176,14 +176,13 @@ __device__ __forceinline__ uint32_t smem_hash(const uint64_t (&c)[W]) {
   return x;
 }
 
-constexpr uint32_t kMapWindows = 1024;  // window → super-mer map per chunk (u8), else binary search
 
 __host__ __device__ constexpr int smem_stage_words(bool pack) { return pack ? 4 : kStageWords; }
 __host__ __device__ constexpr uint32_t smem_overhead(int S) {
-  return 2u * 32u * S * 8u /* forward, double-buffered */ + 32u * S * 8u /* reverse complement */ + kMapWindows;
+  return 2u * 32u * S * 8u /* forward, double-buffered */ + 32u * S * 8u /* reverse complement */;
 }
 
-// Per-warp shared memory: [fwd stage 2][32][S] u64 | [rc stage][32][S] u64 | map u8[1024] |
+// Per-warp shared memory: [fwd stage 2][32][S] u64 | [rc stage][32][S] u64 |
 // table (cap slots) | occupied-slot list u16[cap]
 template <int W, bool PACK>
 __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemCountArgs a, uint32_t warp_bytes) {
@@ -193,12 +192,12 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
   unsigned char* wbase = s_raw + (size_t)wib * warp_bytes;
   uint64_t* stage = reinterpret_cast<uint64_t*>(wbase);              // [2][32 * S]
   uint64_t* rcs = stage + 2 * 32 * S;                                // [32 * S]
-  uint8_t* map = reinterpret_cast<uint8_t*>(rcs + 32 * S);           // [kMapWindows]
+  unsigned char* tab = reinterpret_cast<unsigned char*>(rcs + 32 * S);
   const uint32_t cap = a.cap;
   const uint32_t tail = 2 * a.k - 64 * (W - 1);  // meaningful bits of the last key word
   const uint64_t tmask = tail < 64 ? ~0ull << (64 - tail) : ~0ull;
-  SmemTable<W, PACK> T{map + kMapWindows, cap};
-  uint16_t* occ = reinterpret_cast<uint16_t*>(map + kMapWindows + (size_t)cap * (PACK ? 16u : 8u * W + 4u));
+  SmemTable<W, PACK> T{tab, cap};
+  uint16_t* occ = reinterpret_cast<uint16_t*>(tab + (size_t)cap * (PACK ? 16u : 8u * W + 4u));
   for (uint32_t s = lane; s < cap; s += 32) T.clear(s);
   __syncwarp();
 
@@ -302,25 +301,19 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
           r[u] = rev_pairs(~v);
         }
       }
-      const bool use_map = total <= kMapWindows && !(a.dbg & 2u);
-      if (use_map && nw) {
-        const uint32_t e = incl < kMapWindows ? incl : kMapWindows;
-        for (uint32_t t = excl; t < e; ++t) map[t] = (uint8_t)lane;
-      }
       __syncwarp();
+      // window i → super-mer (lane) j: lanes hold consecutive window ranges [excl, incl)
+      // (empty lanes only at the end of a bin's last chunk), so j = #super-mers starting at
+      // or before i, minus 1 — the round's start bits come from one OR-reduction
+      uint32_t n_before = 0;  // super-mers starting before the current round
       for (uint32_t base = 0; base < total; base += 32) {
         const uint32_t i = base + lane;
         const bool act = i < total;
-        int j = 0;  // super-mer (lane) holding window i
-        if (use_map) {
-          j = act ? map[i] : 31;
-        } else {
-#pragma unroll
-          for (int step = 16; step >= 1; step >>= 1) {
-            const uint32_t v = __shfl_sync(kFull, incl, j + step - 1);
-            if (v <= i) j += step;
-          }
-        }
+        const uint32_t rel = excl - base;
+        const uint32_t starts = __reduce_or_sync(kFull, (nw && rel < 32u) ? 1u << rel : 0u);
+        int j = (int)(n_before + __popc(starts & ((2u << lane) - 1u))) - 1;
+        n_before += __popc(starts);
+        if (!act) j = 31;
         const uint64_t pj = __shfl_sync(kFull, pos, j);
         const uint32_t ej = __shfl_sync(kFull, excl, j);
         const uint32_t Lj = __shfl_sync(kFull, L, j);

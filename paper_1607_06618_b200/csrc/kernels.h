@@ -160,6 +160,7 @@ struct CountArgs {
   uint32_t canonical;        // 1 = count min(x, rc x); 0 = `-d`
 };
 cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
+cudaError_t launch_count_wide(const CountArgs& a, int sms, cudaStream_t s);  // W = 8..15 (count_wide.cu)
 
 // count_smem.cu: steps (d)+(e) for bins whose distinct k-mers fit one warp's
 // shared-memory table (one warp per bin, warp-synchronous inserts, in-place
@@ -227,6 +228,7 @@ struct CountKeysArgs {      // emergency path: insert overflow keys
   TableArgs t;
 };
 cudaError_t launch_count_keys(const CountKeysArgs& a, uint32_t W, int sms, cudaStream_t s);
+cudaError_t launch_count_keys_wide(const CountKeysArgs& a, int sms, cudaStream_t s);
 
 struct CompactArgs {
   unsigned char* table;

@@ -16,14 +16,18 @@
 // edges are merged with atomic OR).
 #include "reader.h"
 
+#include <dlfcn.h>
 #include <fcntl.h>
+#include <zlib.h>
 #include <stdio.h>
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <thread>
 
 namespace gerbil {
@@ -127,6 +131,189 @@ struct Lut {
 };
 static const Lut kLut;
 
+// ---- compressed input (§2.3.1 step 1: reader threads decompress;
+// App. B: "compressed files of these formats") -----------------------
+// gzip (RFC 1952, any number of concatenated members, e.g. BGZF) through zlib; bzip2
+// (any number of concatenated streams) through libbz2, loaded at run time (the image
+// ships the library but no header: the few entry points and bz_stream are declared here).
+bool inflate_gzip(const unsigned char* in, uint64_t len, std::string& out, std::string& err, const char* name) {
+  constexpr uint64_t kPiece = 1u << 30;  // zlib counts in uInt
+  z_stream z{};
+  if (inflateInit2(&z, 15 + 32) != Z_OK) {
+    err = std::string(name) + ": zlib init failed";
+    return false;
+  }
+  out.assign(std::max<uint64_t>(len * 4, 1 << 16), '\0');
+  uint64_t used = 0, fed = 0;  // fed: input bytes handed to zlib so far
+  for (;;) {
+    if (z.avail_in == 0 && fed < len) {
+      const uint64_t n = std::min(len - fed, kPiece);
+      z.next_in = const_cast<Bytef*>(in + fed);
+      z.avail_in = (uInt)n;
+      fed += n;
+    }
+    if (used == out.size()) out.resize(out.size() * 2);
+    const uint64_t room = std::min<uint64_t>(out.size() - used, kPiece);
+    z.next_out = reinterpret_cast<Bytef*>(&out[used]);
+    z.avail_out = (uInt)room;
+    const int r = inflate(&z, Z_NO_FLUSH);
+    used += room - z.avail_out;
+    if (r == Z_STREAM_END) {  // end of one member: another may follow (concatenated gzip / BGZF)
+      uint64_t at = fed - z.avail_in;
+      while (at < len && in[at] == 0) ++at;  // zero padding after the last member
+      if (at >= len) break;
+      inflateReset(&z);
+      const uint64_t n = std::min(len - at, kPiece);
+      z.next_in = const_cast<Bytef*>(in + at);
+      z.avail_in = (uInt)n;
+      fed = at + n;
+      continue;
+    }
+    if (r == Z_BUF_ERROR && z.avail_in == 0 && fed >= len) {
+      inflateEnd(&z);
+      err = std::string(name) + ": truncated gzip stream";
+      return false;
+    }
+    if (r != Z_OK && r != Z_BUF_ERROR) {
+      inflateEnd(&z);
+      err = std::string(name) + ": gzip data error (" + (z.msg ? z.msg : "inflate") + ")";
+      return false;
+    }
+  }
+  inflateEnd(&z);
+  out.resize(used);
+  return true;
+}
+
+struct BzStream {  // bzlib.h bz_stream (stable ABI since bzip2 1.0)
+  char* next_in;
+  unsigned int avail_in, total_in_lo32, total_in_hi32;
+  char* next_out;
+  unsigned int avail_out, total_out_lo32, total_out_hi32;
+  void* state;
+  void* (*bzalloc)(void*, int, int);
+  void (*bzfree)(void*, void*);
+  void* opaque;
+};
+struct Bz2Lib {
+  int (*init)(BzStream*, int, int) = nullptr;
+  int (*step)(BzStream*) = nullptr;
+  int (*end)(BzStream*) = nullptr;
+  bool ok = false;
+  Bz2Lib() {
+    void* h = dlopen("libbz2.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libbz2.so.1.0", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libbz2.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    init = reinterpret_cast<int (*)(BzStream*, int, int)>(dlsym(h, "BZ2_bzDecompressInit"));
+    step = reinterpret_cast<int (*)(BzStream*)>(dlsym(h, "BZ2_bzDecompress"));
+    end = reinterpret_cast<int (*)(BzStream*)>(dlsym(h, "BZ2_bzDecompressEnd"));
+    ok = init && step && end;
+  }
+};
+constexpr int kBzOk = 0, kBzStreamEnd = 4;
+
+bool inflate_bzip2(const unsigned char* in, uint64_t len, std::string& out, std::string& err, const char* name) {
+  static Bz2Lib lib;
+  if (!lib.ok) {
+    err = std::string(name) + ": bzip2 input needs libbz2.so.1";
+    return false;
+  }
+  out.clear();
+  out.resize(std::max<uint64_t>(len * 5, 1 << 16));
+  uint64_t used = 0, pos = 0;
+  while (pos < len) {  // one bzip2 stream per iteration (pbzip2 writes several)
+    BzStream b{};
+    if (lib.init(&b, 0, 0) != kBzOk) {
+      err = std::string(name) + ": bzip2 init failed";
+      return false;
+    }
+    int r = kBzOk;
+    while (r == kBzOk) {
+      if (used == out.size()) out.resize(out.size() * 2);
+      const uint64_t in_chunk = std::min<uint64_t>(len - pos, 1u << 30);
+      const uint64_t room = std::min<uint64_t>(out.size() - used, 1u << 30);
+      b.next_in = const_cast<char*>(reinterpret_cast<const char*>(in + pos));
+      b.avail_in = (unsigned)in_chunk;
+      b.next_out = &out[used];
+      b.avail_out = (unsigned)room;
+      r = lib.step(&b);
+      pos += in_chunk - b.avail_in;
+      used += room - b.avail_out;
+      if (r == kBzOk && in_chunk - b.avail_in == 0 && room - b.avail_out == 0 && pos >= len) r = -7;
+    }
+    lib.end(&b);
+    if (r != kBzStreamEnd) {
+      err = std::string(name) + ": bzip2 data error or truncated stream";
+      return false;
+    }
+    while (pos < len && in[pos] == 0) ++pos;
+  }
+  out.resize(used);
+  return true;
+}
+
+enum class Codec { kPlain, kGzip, kBzip2 };
+Codec sniff(const unsigned char* b, uint64_t len) {
+  if (len >= 2 && b[0] == 0x1f && b[1] == 0x8b) return Codec::kGzip;
+  if (len >= 4 && b[0] == 'B' && b[1] == 'Z' && b[2] == 'h' && b[3] >= '1' && b[3] <= '9') return Codec::kBzip2;
+  return Codec::kPlain;
+}
+
+// one input file as text: mapped when plain, decompressed into `owned` otherwise
+struct FileText {
+  const char* p = nullptr;
+  uint64_t len = 0;
+  void* map = nullptr;
+  uint64_t map_len = 0;
+  std::string owned;
+  std::string err;
+  bool ok = false;
+  ~FileText() {
+    if (map) munmap(map, map_len);
+  }
+};
+
+void load_file(const char* path, FileText& f) {
+  int fd = open(path, O_RDONLY);
+  if (fd < 0) {
+    f.err = std::string(path) + ": cannot open";
+    return;
+  }
+  struct stat st;
+  if (fstat(fd, &st) != 0) {
+    close(fd);
+    f.err = std::string(path) + ": cannot stat";
+    return;
+  }
+  const uint64_t len = (uint64_t)st.st_size;
+  if (len == 0) {
+    close(fd);
+    f.ok = true;
+    return;
+  }
+  void* m = mmap(nullptr, len, PROT_READ, MAP_PRIVATE, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) {
+    f.err = std::string(path) + ": cannot map";
+    return;
+  }
+  const unsigned char* b = (const unsigned char*)m;
+  const Codec c = sniff(b, len);
+  if (c == Codec::kPlain) {
+    f.map = m;
+    f.map_len = len;
+    f.p = (const char*)m;
+    f.len = len;
+    f.ok = true;
+    return;
+  }
+  f.ok = c == Codec::kGzip ? inflate_gzip(b, len, f.owned, f.err, path) : inflate_bzip2(b, len, f.owned, f.err, path);
+  munmap(m, len);
+  f.p = f.owned.data();
+  f.len = f.owned.size();
+}
+
 }  // namespace
 
 bool pack_text(const char* text, uint64_t len, int threads, PackedBatch& out,
@@ -191,35 +378,31 @@ bool pack_text(const char* text, uint64_t len, int threads, PackedBatch& out,
 }
 
 bool pack_file(const char* path, int threads, PackedBatch& out, std::string& err) {
-  int fd = open(path, O_RDONLY);
-  if (fd < 0) {
-    err = std::string(path) + ": cannot open";
-    return false;
+  return pack_files(&path, 1, threads, out, err);
+}
+
+// Files are loaded (mapped, or decompressed — one file per thread, in parallel) ahead of
+// the packer, which appends them in order with all threads.
+bool pack_files(const char* const* paths, uint32_t n, int threads, PackedBatch& out, std::string& err) {
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  std::vector<FileText> files(n);
+  std::atomic<uint32_t> next{0};
+  auto loader = [&] {
+    for (uint32_t i; (i = next.fetch_add(1)) < n;) load_file(paths[i], files[i]);
+  };
+  std::vector<std::thread> ts;
+  const uint32_t nl = std::min<uint32_t>(n, (uint32_t)threads);
+  for (uint32_t t = 1; t < nl; ++t) ts.emplace_back(loader);
+  loader();
+  for (auto& t : ts) t.join();
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!files[i].ok) {
+      err = files[i].err;
+      return false;
+    }
+    if (files[i].len && !pack_text(files[i].p, files[i].len, threads, out, err, paths[i])) return false;
   }
-  struct stat st;
-  if (fstat(fd, &st) != 0) {
-    close(fd);
-    err = std::string(path) + ": cannot stat";
-    return false;
-  }
-  const uint64_t len = (uint64_t)st.st_size;
-  if (len == 0) { close(fd); return true; }
-  void* m = mmap(nullptr, len, PROT_READ, MAP_PRIVATE, fd, 0);
-  close(fd);
-  if (m == MAP_FAILED) {
-    err = std::string(path) + ": cannot map";
-    return false;
-  }
-  const unsigned char* b = (const unsigned char*)m;
-  bool ok;
-  if (len >= 2 && b[0] == 0x1f && b[1] == 0x8b) {
-    err = std::string(path) + ": compressed input is not supported (decompress first)";
-    ok = false;
-  } else {
-    ok = pack_text((const char*)m, len, threads, out, err, path);
-  }
-  munmap(m, len);
-  return ok;
+  return true;
 }
 
 }  // namespace gerbil

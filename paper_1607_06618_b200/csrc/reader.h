@@ -17,5 +17,8 @@ struct PackedBatch {
 bool pack_text(const char* text, uint64_t len, int threads, PackedBatch& out,
                std::string& err, const char* name);
 bool pack_file(const char* path, int threads, PackedBatch& out, std::string& err);
+// Several files, in order; gzip (.gz, concatenated members) and bzip2 inputs are decompressed
+// on host threads (one file per thread).
+bool pack_files(const char* const* paths, uint32_t n, int threads, PackedBatch& out, std::string& err);
 
 }  // namespace gerbil

@@ -44,15 +44,22 @@ constexpr int kThreads = 128;
 constexpr uint32_t kSTile = 1024;  // window positions per tile (also caps super-mer length)
 constexpr int kWarps = kThreads / 32;
 constexpr int kPer = kSTile / kThreads;  // 8 window positions per thread
-constexpr int kMaxK = 200;
-constexpr int kKB = 10;                     // keys per key block (one block per thread)
-constexpr int kKeyLen = kThreads * kKB;     // 1280 >= kSTile + k - m for every k <= 200
 constexpr int kKeyBlocks = kThreads;
-constexpr int kCodeWords = (kKeyLen + 16 + 31) / 32 + 2;          // u64 words of 32 bases
-constexpr int kBitWords = ((kSTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
-constexpr int kBitWords64 = kBitWords / 2;
-static_assert(kKeyLen >= (int)kSTile + kMaxK - 1, "key blocks must cover every window");
-static_assert(kCodeWords + 2 * kBitWords64 <= kThreads, "one staged u64 per thread");
+// Tile geometry for k <= KMAX (two instances: k <= 200 and k <= 479):
+// KB keys per key block (one block per thread), KB * 128 >= kSTile + k - m keys per tile.
+template <int KMAX>
+struct Geo {
+  static constexpr int kMaxK = KMAX;
+  static constexpr int kKB = KMAX <= 200 ? 10 : 12;
+  static constexpr int kKeyLen = kThreads * kKB;
+  static constexpr int kCodeWords = (kKeyLen + 16 + 31) / 32 + 2;          // u64 words of 32 bases
+  static constexpr int kBitWords = ((kSTile + kMaxK + 31) / 32 + 3) & ~1;  // u32 bitmap words (even)
+  static constexpr int kBitWords64 = kBitWords / 2;
+  static_assert(kKeyLen >= (int)kSTile + kMaxK - 1, "key blocks must cover every window");
+  static_assert(kCodeWords + 2 * kBitWords64 <= kThreads, "one staged u64 per thread");
+  static_assert(kKB + 15 - 1 <= 32, "a key block's bases (kKB + m - 1, m <= 15) sit in one u64");
+};
+constexpr int kMaxKSmall = 200, kMaxKAll = 479;
 
 __device__ __forceinline__ bool bget(const uint32_t* bm, uint32_t i) { return (bm[i >> 5] >> (i & 31)) & 1u; }
 
@@ -102,10 +109,13 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #ifndef GERBIL_SM_MINB
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
-template <uint32_t ORD>
+template <uint32_t ORD, int KMAX>
 __global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,
                 int hist_smem) {
+  using G = Geo<KMAX>;
+  constexpr int kKB = G::kKB, kKeyLen = G::kKeyLen, kCodeWords = G::kCodeWords, kBitWords = G::kBitWords,
+                kBitWords64 = G::kBitWords64;
   __shared__ uint64_t s_codes[kCodeWords];
   __shared__ uint32_t s_n[kBitWords];    // N bits
   __shared__ uint32_t s_rs[kBitWords];   // read-start bits
@@ -159,13 +169,16 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
   auto stage_store = [&](uint64_t v) {  // bitmaps: u64 MSB-first → u32 LSB-first
     if (tid < (uint32_t)kCodeWords) {
       s_codes[tid] = v;
-    } else if (tid < (uint32_t)(kCodeWords + 2 * kBitWords64)) {
-      const bool is_n = tid < (uint32_t)(kCodeWords + kBitWords64);
-      const uint32_t i = tid - kCodeWords - (is_n ? 0 : kBitWords64);
-      uint32_t* dst = is_n ? s_n : s_rs;
+    } else if (tid < (uint32_t)(kCodeWords + kBitWords64)) {
+      const uint32_t i = tid - kCodeWords;
       v = __brevll(v);
-      dst[2 * i] = (uint32_t)v;
-      dst[2 * i + 1] = (uint32_t)(v >> 32);
+      s_n[2 * i] = (uint32_t)v;
+      s_n[2 * i + 1] = (uint32_t)(v >> 32);
+    } else if (tid < (uint32_t)(kCodeWords + 2 * kBitWords64)) {
+      const uint32_t i = tid - kCodeWords - kBitWords64;
+      v = __brevll(v);
+      s_rs[2 * i] = (uint32_t)v;
+      s_rs[2 * i + 1] = (uint32_t)(v >> 32);
     }
   };
   uint64_t staged = stage_load(tile_begin + blockIdx.x);
@@ -385,6 +398,7 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
   // and spread global REDs are cheap next to this kernel's arithmetic
   const int hist_smem = a.n_bins <= 2048 && a.bin_windows != nullptr;
   const size_t dyn = hist_smem ? (size_t)nh * a.n_bins * sizeof(uint32_t) : 0;
+  const bool wide = a.k > kMaxKSmall;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
@@ -396,15 +410,18 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
     kern<<<(unsigned)grid, kThreads, dyn, st>>>(a, rs_bits, t0, t1, hist_smem);
     return cudaGetLastError();
   };
+#define GERBIL_SM_ORD(O) \
+  case O: return wide ? go(supermer_kernel<O, kMaxKAll>) : go(supermer_kernel<O, kMaxKSmall>)
   switch (a.ordering) {
-    case kOrdKMC2: return go(supermer_kernel<kOrdKMC2>);
-    case kOrdLEX: return go(supermer_kernel<kOrdLEX>);
-    case kOrdCGAT: return go(supermer_kernel<kOrdCGAT>);
-    case kOrdROBERTS: return go(supermer_kernel<kOrdROBERTS>);
-    case kOrdRANDOM: return go(supermer_kernel<kOrdRANDOM>);
-    case kOrdDFP: return go(supermer_kernel<kOrdDFP>);
+    GERBIL_SM_ORD(kOrdKMC2);
+    GERBIL_SM_ORD(kOrdLEX);
+    GERBIL_SM_ORD(kOrdCGAT);
+    GERBIL_SM_ORD(kOrdROBERTS);
+    GERBIL_SM_ORD(kOrdRANDOM);
+    GERBIL_SM_ORD(kOrdDFP);
     default: return cudaErrorInvalidValue;
   }
+#undef GERBIL_SM_ORD
 }
 
 cudaError_t launch_supermer(const SupermerArgs& a, uint64_t* rs_bits, int sms, cudaStream_t st) {
@@ -420,7 +437,7 @@ uint64_t supermer_tile_count(uint64_t n_bases) { return (n_bases + kSTile - 1) /
 
 // a tile is complete once bases [0, t*kSTile + reach) are resident: its staged
 // code words and bitmap words end below that (kernel step 1)
-uint64_t supermer_tile_reach() { return (uint64_t)kCodeWords * 32 + 64; }
+uint64_t supermer_tile_reach() { return (uint64_t)Geo<kMaxKAll>::kCodeWords * 32 + 64; }  // the larger geometry
 
 uint64_t supermer_scratch_words(uint64_t n_bases) { return (n_bases + 63) / 64 + 2; }
 

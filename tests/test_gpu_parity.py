@@ -1,7 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
 by element on the same seeded inputs — bit-exact sorted (k-mer, count) lists.
 
-Covers every key-word boundary up to k=200, several m / bin counts / thresholds,
+Covers every key-word boundary up to k=479, several m / bin counts / thresholds,
 both read entry points (host reader, device-resident batch), the emergency
 (overflow) path, step (b) properties, invariances and degenerate inputs.
 """
@@ -87,6 +87,27 @@ def test_parity_every_word_boundary(G, k):
     assert st["count_sum"] == ref.windows
 
 
+# k beyond 200, up to the paper's maximum 479 (App. A "-k: Supported k range from
+# 8 to 479"): every key-word boundary of W = 7..15 on 700-bp reads
+KS_WIDE = [201, 223, 224, 225, 256, 257, 300, 383, 384, 385, 448, 449, 479]
+
+
+@pytest.mark.parametrize("k", KS_WIDE)
+def test_parity_wide_keys(G, k):
+    w = synth.Workload(seed=300 + k, genome_len=80_000, read_len=700, n_reads=400, err=0.004, nrate=0.0005)
+    text = synth.fastx(w, synth.FASTA, line_width=80)
+    ref = oracle.count(text, k, 1)
+    with G.Gerbil(n_bins=64) as g:
+        g.count(k, 11, 1, text=text)
+        keys, counts = g.fetch(sorted=True)
+        st = g.stats()
+        binary = g.encode_results(G.FMT_BINARY, sorted=True) if k in (300, 479) else None
+    compare(keys, counts, k, ref)
+    assert st["count_sum"] == ref.windows and st["W"] == (k + 31) // 32
+    if binary is not None:  # App. C records: ceil(k/4) = 75 / 120 key bytes
+        assert binary == b"".join(oracle.encode_entry(x, c) for x, c in zip(ref.kmers, ref.counts))
+
+
 @pytest.mark.parametrize("m,B", [(5, 1), (7, 8), (9, 512), (11, 4096), (15, 100), (3, 7)])
 def test_parity_invariant_in_m_and_bins(G, m, B):
     w = synth.Workload(seed=77, genome_len=30_000, read_len=100, n_reads=3000, err=0.003, nrate=0.001)
@@ -169,9 +190,9 @@ def test_rc_input_doubles_counts_gpu(G):
 
 
 # ---- emergency mechanism ------------------------------------------
-@pytest.mark.parametrize("k", [28, 65, 200])
+@pytest.mark.parametrize("k", [28, 65, 200, 479])
 def test_overflow_path_exact(G, k):
-    w = synth.Workload(seed=21, genome_len=50_000, read_len=250, n_reads=800, err=0.01)
+    w = synth.Workload(seed=21, genome_len=50_000, read_len=max(250, k + 200), n_reads=800, err=0.01)
     text = synth.fastx(w, synth.FASTQ)
     ref = oracle.count(text, k)
     # θ = 1 bucket and an over-full table: many k-mers take the emergency path
@@ -275,7 +296,7 @@ def test_usage_errors(G):
         with pytest.raises(G.GerbilError) as e:
             g.fetch()
         assert e.value.status == G.E_STATE
-        for k, m, l in ((7, 3, 1), (201, 7, 1), (28, 28, 1), (28, 16, 1), (28, 7, 0)):
+        for k, m, l in ((7, 3, 1), (480, 7, 1), (28, 28, 1), (28, 16, 1), (28, 7, 0)):
             with pytest.raises(G.GerbilError) as e:
                 g.count(k, m, l, text=b">a\nACGT\n")
             assert e.value.status == G.E_USAGE
@@ -361,3 +382,27 @@ def test_binary_and_csv_output(G, k, min_count, tmp_path):
     assert max(ref.counts) >= 255
     assert csv == b"".join(x + b"," + str(c).encode() + b"\n" for x, c in zip(ref.kmers, ref.counts))
     assert (tmp_path / "out.bin").read_bytes() == binary
+
+
+# ---- compressed input: gzip / bzip2 files through gerbil_count(paths) --------
+@pytest.mark.parametrize("codec", ["gzip", "bz2"])
+def test_parity_compressed_files(G, codec, tmp_path):
+    import bz2
+    import gzip
+
+    w = synth.Workload(seed=61, genome_len=60_000, read_len=150, n_reads=4000, err=0.004, nrate=0.002)
+    fq = synth.fastx(w, synth.FASTQ)
+    fq2 = synth.fastx(w.shard(0, 2), synth.FASTQ)
+    comp = gzip.compress if codec == "gzip" else bz2.compress
+    paths = [tmp_path / f"a.fq.{codec}", tmp_path / f"b.fq.{codec}"]
+    paths[0].write_bytes(comp(fq))
+    paths[1].write_bytes(comp(fq2))
+    # the harness decompresses with Python's own codec; the oracle counts the plain texts
+    plain = b"".join((gzip.decompress if codec == "gzip" else bz2.decompress)(p.read_bytes()) for p in paths)
+    ref = oracle.count(plain, 40, 1)
+    with G.Gerbil() as g:
+        g.count(40, 11, 1, paths=[str(p) for p in paths])
+        keys, counts = g.fetch(sorted=True)
+        st = g.stats()
+    compare(keys, counts, 40, ref)
+    assert st["count_sum"] == ref.windows

@@ -118,3 +118,50 @@ def test_reader_matches_synth_packing():
     assert np.array_equal(p.read_start, rs)
     assert np.array_equal(p.codes[: len(codes)], codes)
     assert np.array_equal(p.nmask[: len(nmask)], nmask)
+
+
+def test_reader_compressed_inputs(tmp_path):
+    # PAPER.md:94 (§2.3.1 step 1) / App. B: FASTA/FASTQ "and compressed files of
+    # these formats" — gzip (also several concatenated members, as BGZF writes) and bzip2
+    # (also concatenated streams) decode to exactly the plain file's packed batch
+    import bz2
+    import gzip
+
+    from paper_1607_06618_b200 import gerbil
+
+    w = synth.Workload(seed=11, genome_len=40_000, read_len=150, n_reads=900, err=0.01, nrate=0.004)
+    fq = synth.fastx(w, synth.FASTQ)
+    fa = synth.fastx(w, synth.FASTA, line_width=60)
+    plain = tmp_path / "r.fq"
+    plain.write_bytes(fq)
+    ref = gerbil.pack_reads(paths=[str(plain)])
+    half = fq.index(b"\n@", len(fq) // 2) + 1
+    variants = {
+        "r.fq.gz": gzip.compress(fq),
+        "r2.fq.gz": gzip.compress(fq[:half], 1) + gzip.compress(fq[half:], 9),  # two members
+        "r.fq.bz2": bz2.compress(fq),
+        "r2.fq.bz2": bz2.compress(fq[:half]) + bz2.compress(fq[half:]),          # two streams
+    }
+    for name, data in variants.items():
+        f = tmp_path / name
+        f.write_bytes(data)
+        for threads in (1, 4):
+            p = gerbil.pack_reads(paths=[str(f)], threads=threads)
+            assert p.n_reads == ref.n_reads and p.n_bases == ref.n_bases, name
+            assert np.array_equal(p.read_start, ref.read_start), name
+            assert np.array_equal(p.codes, ref.codes) and np.array_equal(p.nmask, ref.nmask), name
+    # several files, mixed codecs, loaded in parallel but packed in order
+    (tmp_path / "a.fa.gz").write_bytes(gzip.compress(fa))
+    both = gerbil.pack_reads(paths=[str(tmp_path / "a.fa.gz"), str(tmp_path / "r.fq.bz2"), str(plain)], threads=3)
+    assert both.n_reads == 3 * ref.n_reads and both.n_bases == 3 * ref.n_bases
+    nb = int(ref.n_bases)
+    assert decode_packed(both.codes, both.nmask, nb, nb) == decode_packed(ref.codes, ref.nmask, 0, nb)
+    assert decode_packed(both.codes, both.nmask, 2 * nb, nb) == decode_packed(ref.codes, ref.nmask, 0, nb)
+    # damaged inputs fail with an I/O error naming the file
+    for name, data in {"t.fq.gz": gzip.compress(fq)[:-40], "c.fq.gz": gzip.compress(fq)[:30] + b"\xff" * 64,
+                       "t.fq.bz2": bz2.compress(fq)[:-30]}.items():
+        f = tmp_path / name
+        f.write_bytes(data)
+        with pytest.raises(gerbil.GerbilError) as e:
+            gerbil.pack_reads(paths=[str(f)])
+        assert name in str(e.value)
