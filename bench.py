@@ -312,6 +312,8 @@ def main() -> None:
     ap.add_argument("--bins", type=int, default=-1)
     ap.add_argument("--m", type=int, default=0, help="minimizer length (results are invariant in m)")
     ap.add_argument("--count-mode", type=int, default=0, help="gerbil_config.count_mode (0 auto, 1 L2, 2 smem)")
+    ap.add_argument("--ordering", type=int, default=-1,
+                    help="minimizer ordering (0 KMC2 .. 5 DFP; default: the config's; results are invariant)")
     args = ap.parse_args()
     set_config(args.config, args.m or None, args.reads or None)
     if args.impl == "reference":
@@ -339,8 +341,9 @@ def main() -> None:
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     n_bins = CFG.n_bins if args.bins < 0 else args.bins
+    ordering = CFG.extra.get("ordering", gerbil.ORDER_KMC2) if args.ordering < 0 else args.ordering
     g = gerbil.Gerbil(device=local, rank=rank, world=world, unique_id=uid, n_bins=n_bins,
-                      stream=stream.cuda_stream, timing=True,
+                      stream=stream.cuda_stream, timing=True, ordering=ordering,
                       wave_table_bytes=args.table_mb << 20, count_mode=args.count_mode)
 
     n_reads = args.reads or CFG.n_reads
@@ -447,6 +450,7 @@ def main() -> None:
             "config": {"workload": WORKLOAD_NAME, "config": CFG.name, "reads_per_gpu": w.n_reads,
                        "read_len": w.read_len, "genome_len": w.genome_len, "err": w.err, "nrate": w.nrate,
                        "k": K, "m": M, "min_count": MIN_COUNT, "n_bins": st["n_bins"], "waves": st["waves"],
+                       "ordering": ["KMC2", "LEX", "CGAT", "ROBERTS", "RANDOM", "DFP"][ordering],
                        "parallelism": f"bins sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (packed reads >= 1.25 GB/GPU); no flush"},
             "kmers_per_s": total_windows / (ms / 1e3),

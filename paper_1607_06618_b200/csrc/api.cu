@@ -331,18 +331,22 @@ gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, ui
                                       uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows,
                                       uint64_t n_bases);
 
-uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, uint32_t m) {
+uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint64_t n_reads, uint32_t W, uint32_t k, uint32_t m) {
   if (ctx->cfg.n_bins) return ctx->cfg.n_bins;
-  // Shared-memory counting (count_smem.cu) wants bins whose distinct k-mers
-  // fit one warp's table: ~0.35 of its slots on average leaves room for
-  // skew. Bins are hashes of minimizers, so that needs many more minimizers
-  // than bins (m >= 11: >= 2M canonical m-mers) — else the L2 policy below.
-  // Measured at C1 scale: the shared-memory path wins for k <= 96 (W <= 3:
-  // 1.1x at k = 40, 1.7x at k = 56, 1.5x at k = 65) and loses for k = 100 (one window per
-  // 100-bp read) and k = 200 (tables too small for its bins) — those keep the L2 policy.
-  const uint32_t cap = (ctx->rec_out || m < 11 || key_words(k) > 3) ? 0u : smem_slots_for(ctx, k);
+  // Shared-memory counting (count_smem.cu for W <= 3, the CTA-wide reference tables of
+  // count_ref.cu for W >= 4) wants bins whose distinct k-mers fit one table: ~0.35 of its
+  // slots on average leaves room for skew. Bins are hashes of minimizers, so that needs many
+  // more minimizers than bins (m >= 11: >= 2M canonical m-mers) — else the L2 policy below.
+  // Windows are estimated from the mean read length (exact for equal-length reads): k = 100 on
+  // 100-bp reads has one window per 100 bases.
+  double windows = (double)n_bases;
+  if (n_reads > 0) {
+    const double len = (double)n_bases / (double)n_reads;
+    windows = std::min(windows, (double)n_reads * std::max(0.0, len - (double)k + 1.0));
+  }
+  const uint32_t cap = (ctx->rec_out || m < 11) ? 0u : smem_slots_for(ctx, k);
   if (cap) {
-    const double want = ctx->rho * (double)n_bases * ctx->world / (0.35 * cap);
+    const double want = ctx->rho * windows / (0.35 * cap);
     uint32_t B = 512;
     while ((double)B < want && B < (1u << 22)) B <<= 1;
     while (B < 64u * (uint32_t)ctx->world) B <<= 1;
@@ -352,7 +356,7 @@ uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint32_t W, uint32_t k, 
   // whole bins), at least 512 (the paper's default F) and at
   // least 64 per rank.
   const double slot = 8.0 + 8.0 * W;
-  const double table = ctx->rho * (double)n_bases * ctx->world * slot / ctx->cfg.target_load;
+  const double table = ctx->rho * windows * slot / ctx->cfg.target_load;
   const double per_bin = (double)ctx->cfg.wave_table_bytes / 16.0;
   uint32_t B = 512;
   while ((double)B * per_bin < table && B < 8192) B <<= 1;
@@ -491,9 +495,24 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
     const uint64_t lane_bytes = (max_nb * bb + 255) & ~255ull;
     CK(ctx->table.ensure(lanes * lane_bytes));
     CK(ctx->ovf.ensure(ovf_cap * W * 8));
-    const uint64_t out_cap = pre.out_n + out_bound + ovf_cap;
+    // Result buffer: the waves' distinct bound can exceed device memory when most k-mers are
+    // singletons and min_count > 1 drops them (C4: ~1.5e10 bound, ~3.6e8 kept per GPU), so it is
+    // sized for at most a quarter of the free memory and grown between waves when the bound of
+    // the next wave might not fit (a sync reads how many results the earlier waves kept).
+    uint64_t out_chunk = out_bound;
+    {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+        const uint64_t fit = (uint64_t)(fr / 4) / (W * 8 + 4);
+        uint64_t big_wave = 0;
+        for (const Wave& wv : waves) big_wave = std::max(big_wave, std::min<uint64_t>(wv.nb * kSlotsPerBucket, wv.windows));
+        out_chunk = std::min(out_bound, std::max(fit, 2 * big_wave));
+      }
+    }
+    uint64_t out_cap = pre.out_n + out_chunk + ovf_cap;
     CK(ensure_keep(ctx->out_keys, out_cap * W * 8, pre.out_n * W * 8, ctx->stream));
     CK(ensure_keep(ctx->out_counts, out_cap * 4, pre.out_n * 4, ctx->stream));
+    uint64_t out_committed = pre.out_n, bound_left = out_bound;  // results possibly written / still to come
     // [0, n): distinct per wave; [n, 2n): dynamic work counters of the count launches
     const size_t nw = std::max<size_t>(waves.size(), 1);
     CK(ctx->wave_distinct.ensure(2 * nw * 8));
@@ -605,11 +624,34 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
       for (size_t w = 0; w < waves.size(); ++w) {
         const int lane = two ? (int)(w & 1) : 0;
         cudaStream_t st = lane ? ctx->lane_stream : ctx->stream;
+        const uint64_t wb = std::min<uint64_t>(waves[w].nb * kSlotsPerBucket, waves[w].windows);
+        if (!streaming && out_committed + wb + ovf_cap > out_cap) {
+          // the next wave might not fit: settle how many results the launched waves kept
+          if (two) CK(cudaStreamSynchronize(ctx->lane_stream));
+          CK(cudaMemcpyAsync(&hc.out_n, &dc->out_n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+          CK(cudaStreamSynchronize(ctx->stream));
+          out_committed = hc.out_n;
+          if (out_committed + wb + ovf_cap > out_cap) {
+            out_cap = out_committed + std::max(std::min(bound_left, out_chunk), wb) + ovf_cap;
+            CK(ensure_keep(ctx->out_keys, out_cap * W * 8, out_committed * W * 8, ctx->stream));
+            CK(ensure_keep(ctx->out_counts, out_cap * 4, out_committed * 4, ctx->stream));
+            ca.out_keys = ctx->out_keys.as<uint64_t>();
+            ca.out_counts = ctx->out_counts.as<uint32_t>();
+            ca.cap = out_cap;
+          }
+          if (two) {  // the lane stream continues after everything issued on the main stream
+            CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->lane_stream, ctx->fork_ev, 0));
+          }
+        }
+        out_committed += wb;
+        bound_left -= std::min(bound_left, wb);
         t.table = ctx->table.as<unsigned char>() + lane * lane_bytes;
         t.nb = waves[w].nb;
         CountArgs a{stream_codes, desc, waves[w].d0, waves[w].d1, k, t,
                     ctx->wave_distinct.as<unsigned long long>() + nw + w,
-                    ctx->cfg.disable_normalization ? 0u : 1u};
+                    ctx->cfg.disable_normalization ? 0u : 1u,
+                    count_dpc((double)waves[w].windows / (double)std::max<uint64_t>(1, waves[w].d1 - waves[w].d0))};
         {
           Timer tm(ctx, K_COUNT, st, !two);
           CK(launch_count(a, W, ctx->sms, st));
@@ -739,19 +781,23 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
 
 // Shared-memory table slots per warp for this k (0 = shared-memory path off).
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
-  if (ctx->cfg.count_mode == 1 || key_words(k) > 7) return 0;  // shared-memory tables: W <= 7
+  if (ctx->cfg.count_mode == 1) return 0;
   if (!ctx->smem_optin &&
       cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  const uint32_t cap = smem_table_slots(k, (size_t)ctx->smem_optin - 1024);
+  // W >= 4: one CTA-wide table of occurrence references per bin (count_ref.cu)
+  const uint32_t cap = key_words(k) >= 4 ? ref_table_slots((size_t)ctx->smem_optin - 1024)
+                                         : smem_table_slots(k, (size_t)ctx->smem_optin - 1024);
   return cap >= 128 ? cap : 0;
 }
 
 // Abandonment threshold of the shared-memory tables: a round inserts <= 32 k-mers, so
 // a table never fills.
-uint32_t smem_max_fill(uint32_t cap) { return cap - std::max<uint32_t>(64u, cap / 4); }
+uint32_t smem_max_fill(uint32_t cap, uint32_t k) {
+  return key_words(k) >= 4 ? ref_max_fill(cap) : cap - std::max<uint32_t>(64u, cap / 4);
+}
 
 // Windows up to which a bin goes to the shared-memory pass: predicted distinct
 // (ρ̂ · windows) within the abandonment threshold; a miss costs only the bin's
@@ -775,8 +821,17 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
                                  uint64_t total_windows) {
   const uint32_t W = key_words(k);
   CK(ctx->smem_failed.ensure((size_t)n * 16 + 16));
-  CK(ctx->out_keys.ensure(std::max<uint64_t>(out_bound, 1) * W * 8));
-  CK(ctx->out_counts.ensure(std::max<uint64_t>(out_bound, 1) * 4));
+  // the shared-memory pass writes at most out_bound results, but with min_count > 1 on singleton-rich
+  // input (C4) that bound can exceed device memory: the buffer is capped at a quarter of the free
+  // memory and, if the kept results do not fit, the pass is rerun once with the exact size
+  uint64_t out_cap = std::max<uint64_t>(out_bound, 1);
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+      out_cap = std::min<uint64_t>(out_cap, std::max<uint64_t>(1, (uint64_t)(fr / 4) / (W * 8 + 4)));
+  }
+  CK(ctx->out_keys.ensure(out_cap * W * 8));
+  CK(ctx->out_counts.ensure(out_cap * 4));
   CK(ctx->counters.ensure(sizeof(Counters)));
   Counters* dc = ctx->counters.as<Counters>();
   CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
@@ -790,24 +845,32 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   a.canonical = ctx->cfg.disable_normalization ? 0u : 1u;
   a.cap = cap;
   a.max_fill = max_fill;
-  a.out_keys = ctx->out_keys.as<uint64_t>();
-  a.out_counts = ctx->out_counts.as<uint32_t>();
-  a.out_cap = out_bound;
   a.out_n = &dc->out_n;
   a.sum_counts = &dc->sum_counts;
   a.distinct = &dc->distinct;
   a.failed = ctx->smem_failed.as<unsigned long long>();
   a.n_failed = &dc->read_work;
-  {
-    Timer tm(ctx, K_SMEM);
-    CK(launch_count_smem(a, ctx->sms, ctx->stream));
-  }
-  trace("smem count issued");
   Counters& hc = *ctx->h_counters;
-  CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  trace("smem count done (synced)");
-  if (hc.out_n > out_bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+  for (int attempt = 0;; ++attempt) {
+    a.out_keys = ctx->out_keys.as<uint64_t>();
+    a.out_counts = ctx->out_counts.as<uint32_t>();
+    a.out_cap = out_cap;
+    {
+      Timer tm(ctx, K_SMEM);
+      CK(launch_count_smem(a, ctx->sms, ctx->stream));
+    }
+    trace("smem count issued");
+    CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    trace("smem count done (synced)");
+    if (hc.out_n > out_bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+    if (hc.out_n <= out_cap) break;
+    if (attempt > 0) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory pass: result size changed on rerun");
+    out_cap = hc.out_n;  // exact: the rerun keeps the same k-mers
+    CK(ctx->out_keys.ensure(out_cap * W * 8));
+    CK(ctx->out_counts.ensure(out_cap * 4));
+    CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
+  }
   const uint64_t n_failed = hc.read_work;
   Preset pre;
   pre.out_n = hc.out_n;
@@ -833,7 +896,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   const int w2n = std::max(1, w1 / 2);
   const uint32_t cap2 = w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u;
   if (!rest.empty() && cap2 > cap) {
-    const uint32_t mf2 = smem_max_fill(cap2);
+    const uint32_t mf2 = smem_max_fill(cap2, k);
     const uint64_t thr2 = smem_window_threshold(ctx, mf2);
     std::vector<RestBin> keep;
     uint64_t n2 = 0, w2 = 0, ob2 = 0;
@@ -958,7 +1021,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   ctx->stats.smem_slots = cap;
   if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
                                       total_windows, Preset{});
-  const uint32_t max_fill = smem_max_fill(cap);
+  const uint32_t max_fill = smem_max_fill(cap, k);
   const uint64_t thr = smem_window_threshold(ctx, max_fill);
   std::vector<uint32_t> elig;
   std::vector<RestBin> rest;
@@ -997,40 +1060,167 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
 // device — exclusive scan of the per-bin super-mer counts (bin offsets), scatter, and
 // the split into the shared-memory list and the rest (plan_bins_kernel); only the
 // rest bins (few) come to the host for the wave tables.
+// (c) on one rank: group-major shuffle (shuffle.cu) of desc_in/bin_in into ctx->desc_sorted; the
+// bins' offsets (ctx->bin_off_d) and windows (ctx->hist) come out of it. tmp_* are scratch of n.
+gerbil_status group_shuffle(gerbil_ctx* ctx, const uint64_t* desc_in, const uint32_t* bin_in, uint64_t n, uint32_t B,
+                            uint64_t* tmp_desc, uint32_t* tmp_bin, uint64_t* desc_alt) {
+  if (n >= (1ull << 32)) return fail(ctx, GERBIL_E_USAGE, "more than 2^32 super-mers in one call: split the batch");
+  CK(ctx->hist.ensure(3ull * B * 8));
+  CK(ctx->bin_off_d.ensure(((size_t)B + 1) * 8));
+  CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n, 1) * 8));
+  CK(ctx->p_tmp.ensure(group_shuffle_scratch_bytes(B)));
+  GroupShuffleArgs gs{};
+  gs.desc_in = desc_in;
+  gs.bin_in = bin_in;
+  gs.n = n;
+  gs.n_bins = B;
+  gs.tmp_desc = tmp_desc;
+  gs.tmp_bin = tmp_bin;
+  gs.desc_alt = desc_alt;
+  gs.desc_out = ctx->desc_sorted.as<uint64_t>();
+  gs.off = ctx->bin_off_d.as<unsigned long long>();
+  gs.win = ctx->hist.as<unsigned long long>();
+  gs.scratch = ctx->p_tmp.as<unsigned long long>();
+  const uint32_t G = group_shuffle_groups(B);
+  Timer tm(ctx, K_SHUFFLE, nullptr, true, G > 64 ? 5 : 4);
+  CK(launch_group_shuffle(gs, ctx->sms, ctx->stream));
+  return GERBIL_OK;
+}
+
+gerbil_status count_planned(gerbil_ctx* ctx, const uint64_t* codes, uint32_t B, uint32_t cap, uint32_t k,
+                            uint32_t min_count, uint64_t windows);
+
 gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
                                       uint32_t cap, uint32_t k, uint32_t min_count, uint64_t windows,
                                       uint64_t n_bases) {
-  ctx->stats.smem_slots = cap;
   (void)n_bases;
-  if (n_sm >= (1ull << 32))
-    return fail(ctx, GERBIL_E_USAGE, "more than 2^32 super-mers in one call: split the batch");
-  // (c): group-major shuffle (shuffle.cu) — bins' offsets and windows come out of it
-  unsigned long long* d_win = ctx->hist.as<unsigned long long>();
-  CK(ctx->bin_off_d.ensure(((size_t)B + 1) * 8));
-  unsigned long long* d_off = ctx->bin_off_d.as<unsigned long long>();
-  CK(ctx->desc_sorted.ensure(std::max<uint64_t>(n_sm, 1) * 8));
   CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));  // scratch (reuses the exchange buffers)
   CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
-  CK(ctx->p_tmp.ensure(group_shuffle_scratch_bytes(B)));
-  GroupShuffleArgs gs{};
-  gs.desc_in = ctx->desc_pre.as<uint64_t>();
-  gs.bin_in = ctx->bin_pre.as<uint32_t>();
-  gs.n = n_sm;
-  gs.n_bins = B;
-  gs.tmp_desc = ctx->send_desc.as<uint64_t>();
-  gs.tmp_bin = ctx->send_bin.as<uint32_t>();
-  gs.desc_alt = ctx->desc_pre.as<uint64_t>();
-  gs.desc_out = ctx->desc_sorted.as<uint64_t>();
-  gs.off = d_off;
-  gs.win = d_win;
-  gs.scratch = ctx->p_tmp.as<unsigned long long>();
+  CKS(group_shuffle(ctx, ctx->desc_pre.as<uint64_t>(), ctx->bin_pre.as<uint32_t>(), n_sm, B,
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>()));
+  return count_planned(ctx, codes, B, cap, k, min_count, windows);
+}
+
+// Step (c) across ranks with the device bin plan kept (many bins, shared-memory / reference
+// tables): every rank groups its super-mers by bin (group_shuffle), bins are owned in GROUPS of
+// 1024 consecutive bins (4096 groups at 2^22 bins) so the plan is small: the per-group windows /
+// super-mers / payload words of all ranks are all-gathered (3 x 32 KB per rank) and every rank
+// derives the same greedy LPT owner map (exchange_plan over groups; PAPER.md:210's load balance,
+// all occurrences of a k-mer end up on one GPU). Each rank packs its groups into
+// per-destination segments (descriptor with the position already rebased into the owner's receive
+// buffer, bin, re-aligned payload) and ONE grouped ncclSend/ncclRecv moves all three; the owner
+// regroups what it received by bin and counts it with the device plan (count_planned).
+gerbil_status exchange_groups(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B, uint32_t cap,
+                              uint32_t k, uint32_t min_count, uint64_t& owned_windows) {
+  const int P = ctx->world, r = ctx->rank;
+  const uint32_t G = group_shuffle_groups(B);
+  CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));
+  CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
+  CKS(group_shuffle(ctx, ctx->desc_pre.as<uint64_t>(), ctx->bin_pre.as<uint32_t>(), n_sm, B,
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>()));
+  // per-group statistics of every rank
+  CK(ctx->hist_all.ensure(3ull * G * 8 * (P + 1)));
+  unsigned long long* gst = ctx->hist_all.as<unsigned long long>();
+  unsigned long long* gall = gst + 3ull * G;
   {
-    const uint32_t G = group_shuffle_groups(B);
-    Timer tm(ctx, K_SHUFFLE, nullptr, true, G > 64 ? 5 : 4);
-    CK(launch_group_shuffle(gs, ctx->sms, ctx->stream));
+    Timer tm(ctx, K_SHUFFLE);
+    CK(launch_group_stats(ctx->desc_sorted.as<uint64_t>(), ctx->bin_off_d.as<unsigned long long>(), B, k, gst,
+                          ctx->stream));
   }
+  if (!ctx->comm->allgather(gst, gall, 3ull * G * 8, ctx->stream)) return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+  std::vector<uint64_t> H(3ull * G * P);
+  CK(cudaMemcpyAsync(H.data(), gall, H.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  trace("group histograms all-gathered");
+  auto Hw = [&](int s, uint32_t g) { return H[(size_t)s * 3 * G + g]; };
+  auto Hc = [&](int s, uint32_t g) { return H[(size_t)s * 3 * G + G + g]; };
+  auto Hp = [&](int s, uint32_t g) { return H[(size_t)s * 3 * G + 2 * G + g]; };
+  std::vector<int32_t> owner(G);
+  std::vector<uint64_t> sd_off(P + 1), sw_off(P + 1), rd_off(P + 1), rw_off(P + 1);
+  exchange_plan(H.data(), G, P, r, owner.data(), sd_off.data(), sw_off.data(), rd_off.data(), rw_off.data());
+  // this rank's data starts, in destination d's receive buffer, after the lower ranks' data
+  std::vector<uint64_t> rb(P, 0);
+  for (int s = 0; s < r; ++s)
+    for (uint32_t g = 0; g < G; ++g) rb[owner[g]] += Hp(s, g);
+  std::vector<unsigned long long> base3(3ull * G);
+  {
+    std::vector<uint64_t> cd(sd_off.begin(), sd_off.end() - 1), cw(sw_off.begin(), sw_off.end() - 1);
+    for (uint32_t g = 0; g < G; ++g) {
+      const int d = owner[g];
+      base3[g] = cd[d];
+      base3[G + g] = cw[d];
+      base3[2ull * G + g] = rb[d] + (cw[d] - sw_off[d]);
+      cd[d] += Hc(r, g);
+      cw[d] += Hp(r, g);
+    }
+  }
+  owned_windows = 0;
+  uint64_t max_group = 0;
+  for (uint32_t g = 0; g < G; ++g)
+    if (owner[g] == r) {
+      uint64_t w = 0;
+      for (int s = 0; s < P; ++s) w += Hw(s, g);
+      owned_windows += w;
+      max_group = std::max(max_group, w);
+    }
+  const uint64_t n_send = sd_off[P], w_send = sw_off[P], n_recv = rd_off[P], w_recv = rw_off[P];
+  CK(ctx->seg_base.ensure(3ull * G * 8));
+  CK(cudaMemcpyAsync(ctx->seg_base.p, base3.data(), base3.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(ctx->send_desc.ensure(std::max<uint64_t>(std::max(n_send, n_recv), 1) * 8));
+  CK(ctx->send_bin.ensure(std::max<uint64_t>(std::max(n_send, n_recv), 1) * 4));
+  CK(ctx->send_payload.ensure(std::max<uint64_t>(w_send, 1) * 8));
+  CK(ctx->recv_desc.ensure(std::max<uint64_t>(n_recv, 1) * 8));
+  CK(ctx->recv_bin.ensure(std::max<uint64_t>(n_recv, 1) * 4));
+  CK(ctx->recv_payload.ensure(std::max<uint64_t>(w_recv, 1) * 8));
+  {
+    Timer tm(ctx, K_SHUFFLE);
+    CK(launch_group_pack(ctx->desc_sorted.as<uint64_t>(), ctx->bin_off_d.as<unsigned long long>(), B, codes, k,
+                         ctx->seg_base.as<unsigned long long>(), ctx->send_desc.as<uint64_t>(),
+                         ctx->send_bin.as<uint32_t>(), ctx->send_payload.as<uint64_t>(), ctx->stream));
+  }
+  // one grouped all-to-all: descriptors, bins and payload to every owner
+  std::vector<size_t> so[3], sb[3], ro[3], rbytes[3];
+  const std::vector<uint64_t>* soff[3] = {&sd_off, &sd_off, &sw_off};
+  const std::vector<uint64_t>* roff[3] = {&rd_off, &rd_off, &rw_off};
+  const size_t elem[3] = {8, 4, 8};
+  Comm::Xfer x[3];
+  void* sbuf[3] = {ctx->send_desc.p, ctx->send_bin.p, ctx->send_payload.p};
+  void* rbuf[3] = {ctx->recv_desc.p, ctx->recv_bin.p, ctx->recv_payload.p};
+  for (int b = 0; b < 3; ++b) {
+    so[b].resize(P);
+    sb[b].resize(P);
+    ro[b].resize(P);
+    rbytes[b].resize(P);
+    for (int p = 0; p < P; ++p) {
+      so[b][p] = (*soff[b])[p] * elem[b];
+      sb[b][p] = ((*soff[b])[p + 1] - (*soff[b])[p]) * elem[b];
+      ro[b][p] = (*roff[b])[p] * elem[b];
+      rbytes[b][p] = ((*roff[b])[p + 1] - (*roff[b])[p]) * elem[b];
+    }
+    x[b] = Comm::Xfer{sbuf[b], so[b].data(), sb[b].data(), rbuf[b], ro[b].data(), rbytes[b].data()};
+  }
+  {
+    Timer tm(ctx, K_SHUFFLE);
+    if (!ctx->comm->alltoallv_multi(x, 3, ctx->stream)) return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+  }
+  trace("groups exchanged");
+  ctx->stats.bytes_sent = (n_send - (sd_off[r + 1] - sd_off[r])) * 12 + (w_send - (sw_off[r + 1] - sw_off[r])) * 8;
+  ctx->stats.bytes_recv = (n_recv - (rd_off[r + 1] - rd_off[r])) * 12 + (w_recv - (rw_off[r + 1] - rw_off[r])) * 8;
+  // regroup what this rank owns by bin, then count it
+  CKS(group_shuffle(ctx, ctx->recv_desc.as<uint64_t>(), ctx->recv_bin.as<uint32_t>(), n_recv, B,
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->recv_desc.as<uint64_t>()));
+  return count_planned(ctx, ctx->recv_payload.as<uint64_t>(), B, cap, k, min_count, owned_windows);
+}
+
+// Steps (d)+(e) over ctx->desc_sorted with the bins' offsets / windows on the device (after
+// group_shuffle): the device bin plan, shared-memory (or reference) tables, then the L2 waves.
+gerbil_status count_planned(gerbil_ctx* ctx, const uint64_t* codes, uint32_t B, uint32_t cap, uint32_t k,
+                            uint32_t min_count, uint64_t windows) {
+  ctx->stats.smem_slots = cap;
+  unsigned long long* d_win = ctx->hist.as<unsigned long long>();
+  unsigned long long* d_off = ctx->bin_off_d.as<unsigned long long>();
   trace("scatter issued");
-  const uint32_t max_fill = smem_max_fill(cap);
+  const uint32_t max_fill = smem_max_fill(cap, k);
   CK(ctx->smem_range.ensure((size_t)B * 16));
   CK(ctx->rest_range.ensure((size_t)B * 24));
   CK(ctx->plan_sums.ensure(5 * 8));
@@ -1252,11 +1442,25 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
     CK(cudaStreamSynchronize(ctx->stream));
     n_bases = ctx->h_counters->probe[3];
   }
-  // all ranks must agree on B: derive it from the largest local batch
-  uint64_t nb_for_bins = n_bases;
-  const uint32_t B = choose_bins(ctx, nb_for_bins, W, k, m);
-  if (ctx->world > 1 && ctx->cfg.n_bins == 0)
-    return fail(ctx, GERBIL_E_USAGE, "world > 1 requires an explicit n_bins (identical on all ranks)");
+  // all ranks must agree on B: it is derived from the job's totals (all-gathered sizes)
+  uint64_t tot_bases = n_bases, tot_reads = n_reads;
+  if (ctx->comm && ctx->cfg.n_bins == 0) {
+    CK(ctx->plan_sums.ensure(2ull * 8 * (ctx->world + 1)));
+    uint64_t* sz = ctx->plan_sums.as<uint64_t>();
+    ctx->h_counters->probe[0] = n_bases;
+    ctx->h_counters->probe[1] = n_reads;
+    CK(cudaMemcpyAsync(sz, ctx->h_counters->probe, 16, cudaMemcpyHostToDevice, ctx->stream));
+    if (!ctx->comm->allgather(sz, sz + 2, 16, ctx->stream)) return fail(ctx, GERBIL_E_NCCL, ctx->comm->err);
+    std::vector<uint64_t> all(2ull * ctx->world);
+    CK(cudaMemcpyAsync(all.data(), sz + 2, all.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    tot_bases = tot_reads = 0;
+    for (int p = 0; p < ctx->world; ++p) {
+      tot_bases += all[2 * p];
+      tot_reads += all[2 * p + 1];
+    }
+  }
+  const uint32_t B = choose_bins(ctx, tot_bases, tot_reads, W, k, m);
   CK(ctx->counters.ensure(sizeof(Counters)));
   CK(ctx->hist.ensure(3ull * B * 8));
   ctx->stats.n_bins = B;
@@ -1264,10 +1468,12 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   ctx->stats.input_bases = n_bases;
   ctx->stats.input_reads = n_reads;
 
-  // the device-planned path (single rank, many bins) groups super-mers with the group-major
-  // shuffle, which derives the bin histogram itself: step (b) then skips it
-  const uint32_t smem_cap = (!ctx->comm && !ctx->rec_out && B >= kDevicePlanBins && B <= (1u << 22) &&
-                             n_bases < (1ull << 43))
+  // the device-planned path (many bins) groups super-mers with the group-major shuffle, which
+  // derives the bin histogram itself: step (b) then skips it. With world > 1 whole groups of
+  // bins are exchanged (exchange_groups) and each owner plans its bins on the device.
+  const uint64_t pos_lim = key_words(k) >= 4 ? (1ull << 39) : (1ull << 43);
+  const uint32_t smem_cap = (!ctx->rec_out && B >= kDevicePlanBins && B <= (1u << 22) && n_bases < pos_lim &&
+                             (!ctx->comm || tot_bases < pos_lim))
                                 ? smem_slots_for(ctx, k)
                                 : 0u;
   // (b)
@@ -1279,7 +1485,10 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   ctx->stats.supermers = n_sm;
   ctx->stats.valid_windows = local_windows;
   uint64_t owned_windows = 0;
-  if (smem_cap) {
+  if (smem_cap && ctx->comm) {
+    // many bins, several ranks: groups of bins exchanged, then planned on the device by the owner
+    CKS(exchange_groups(ctx, codes, n_sm, B, smem_cap, k, min_count, owned_windows));
+  } else if (smem_cap) {
     // many bins, one rank: steps (c)-(e) planned on the device (no per-bin host work)
     CKS(count_local_device_plan(ctx, codes, n_sm, B, smem_cap, k, min_count, local_windows, n_bases));
     owned_windows = local_windows;

@@ -9,8 +9,11 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <map>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -32,6 +35,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   const char* (*GetErrorString)(ncclResult_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);  // optional
+  ncclResult_t (*CommAbort)(ncclComm_t);                          // optional
 };
 
 NcclApi* nccl_api(std::string& err) {
@@ -44,7 +49,7 @@ NcclApi* nccl_api(std::string& err) {
     if (!h) return;
 #define SYM(n) api.n = reinterpret_cast<decltype(api.n)>(dlsym(h, "nccl" #n))
     SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(AllGather); SYM(Send);
-    SYM(Recv); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString);
+    SYM(Recv); SYM(GroupStart); SYM(GroupEnd); SYM(GetErrorString); SYM(CommGetAsyncError); SYM(CommAbort);
 #undef SYM
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
              api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
@@ -68,21 +73,75 @@ class NcclComm : public Comm {
     err = std::string(what) + ": " + api->GetErrorString(r);
     return false;
   }
+  // Wait for the collective on st, polling NCCL's asynchronous error state; a peer that never
+  // arrives (dead rank) ends in a timeout (GERBIL_NCCL_TIMEOUT_S, default 600 s) and an abort,
+  // so the call fails instead of hanging.
+  bool wait(cudaStream_t st, const char* what) {
+    static const double limit = [] {
+      const char* e = getenv("GERBIL_NCCL_TIMEOUT_S");
+      return (e && *e) ? atof(e) : 600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) return true;
+      if (q != cudaErrorNotReady) {
+        err = std::string(what) + ": " + cudaGetErrorString(q);
+        return false;
+      }
+      if (api->CommGetAsyncError) {
+        ncclResult_t ae = ncclSuccess;
+        if (api->CommGetAsyncError(comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress) {
+          err = std::string(what) + ": asynchronous NCCL error: " + api->GetErrorString(ae);
+          if (api->CommAbort) api->CommAbort(comm);
+          comm = nullptr;
+          return false;
+        }
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+        err = std::string(what) + ": timed out waiting for the peers (GERBIL_NCCL_TIMEOUT_S)";
+        if (api->CommAbort) api->CommAbort(comm);
+        comm = nullptr;
+        return false;
+      }
+      if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   bool allgather(const void* s, void* r, size_t bytes, cudaStream_t st) override {
+    if (!comm) {
+      err = "NCCL communicator aborted by an earlier error";
+      return false;
+    }
     if (!check(api->AllGather(s, r, bytes, ncclUint8, comm, st), "ncclAllGather")) return false;
-    return cudaStreamSynchronize(st) == cudaSuccess;
+    return wait(st, "ncclAllGather");
   }
   bool alltoallv(const void* s, const size_t* so, const size_t* sb, void* r, const size_t* ro,
                  const size_t* rb, cudaStream_t st) override {
-    if (!check(api->GroupStart(), "ncclGroupStart")) return false;
-    for (int p = 0; p < world; ++p) {
-      if (sb[p] && !check(api->Send((const char*)s + so[p], sb[p], ncclUint8, p, comm, st), "ncclSend"))
-        return false;
-      if (rb[p] && !check(api->Recv((char*)r + ro[p], rb[p], ncclUint8, p, comm, st), "ncclRecv"))
-        return false;
+    Xfer x{s, so, sb, r, ro, rb};
+    return alltoallv_multi(&x, 1, st);
+  }
+  bool alltoallv_multi(const Xfer* x, int n, cudaStream_t st) override {
+    if (!comm) {
+      err = "NCCL communicator aborted by an earlier error";
+      return false;
     }
+    if (!check(api->GroupStart(), "ncclGroupStart")) return false;
+    for (int p = 0; p < world; ++p)
+      for (int b = 0; b < n; ++b) {
+        const size_t sb = x[b].send_bytes[p], rb = x[b].recv_bytes[p];
+        if (sb && !check(api->Send((const char*)x[b].send + x[b].send_off[p], sb, ncclUint8, p, comm, st),
+                         "ncclSend")) {
+          api->GroupEnd();
+          return false;
+        }
+        if (rb && !check(api->Recv((char*)x[b].recv + x[b].recv_off[p], rb, ncclUint8, p, comm, st),
+                         "ncclRecv")) {
+          api->GroupEnd();
+          return false;
+        }
+      }
     if (!check(api->GroupEnd(), "ncclGroupEnd")) return false;
-    return cudaStreamSynchronize(st) == cudaSuccess;
+    return wait(st, "grouped ncclSend/ncclRecv");
   }
 };
 
@@ -129,20 +188,26 @@ class LoopComm : public Comm {
   }
   bool alltoallv(const void* s, const size_t* so, const size_t* sb, void* r, const size_t* ro,
                  const size_t* rb, cudaStream_t st) override {
-    g->send[rank] = s;
-    g->soff[rank] = so;
-    g->sbytes[rank] = sb;
-    g->barrier();
+    Xfer x{s, so, sb, r, ro, rb};
+    return alltoallv_multi(&x, 1, st);
+  }
+  bool alltoallv_multi(const Xfer* x, int n, cudaStream_t st) override {
     bool ok = true;
-    for (int p = 0; p < world; ++p) {
-      size_t n = g->sbytes[p][rank];
-      if (n != rb[p]) ok = false;
-      if (n && ok)
-        ok &= cudaMemcpyAsync((char*)r + ro[p], (const char*)g->send[p] + g->soff[p][rank], n,
-                              cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+    for (int b = 0; b < n; ++b) {
+      g->send[rank] = x[b].send;
+      g->soff[rank] = x[b].send_off;
+      g->sbytes[rank] = x[b].send_bytes;
+      g->barrier();
+      for (int p = 0; p < world; ++p) {
+        const size_t m = g->sbytes[p][rank];
+        if (m != x[b].recv_bytes[p]) ok = false;
+        if (m && ok)
+          ok &= cudaMemcpyAsync((char*)x[b].recv + x[b].recv_off[p], (const char*)g->send[p] + g->soff[p][rank], m,
+                                cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+      }
+      ok &= cudaStreamSynchronize(st) == cudaSuccess;
+      g->barrier();
     }
-    ok &= cudaStreamSynchronize(st) == cudaSuccess;
-    g->barrier();
     if (!ok) err = "loopback alltoallv size mismatch or copy failure";
     return ok;
   }

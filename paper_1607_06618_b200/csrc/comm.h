@@ -20,6 +20,16 @@ class Comm {
   virtual bool alltoallv(const void* d_send, const size_t* send_off, const size_t* send_bytes,
                          void* d_recv, const size_t* recv_off, const size_t* recv_bytes,
                          cudaStream_t s) = 0;
+  // Several all-to-allv exchanges issued as ONE grouped send/recv (NCCL group): buffer b of
+  // every peer p is sent from send[b] + send_off[b][p] (send_bytes[b][p] bytes) and received
+  // at recv[b] + recv_off[b][p]. Blocking; NCCL errors and a stalled peer (timeout) fail it.
+  struct Xfer {
+    const void* send;
+    const size_t *send_off, *send_bytes;
+    void* recv;
+    const size_t *recv_off, *recv_bytes;
+  };
+  virtual bool alltoallv_multi(const Xfer* x, int n, cudaStream_t s) = 0;
 };
 
 // backend 0 = NCCL (dlopen'ed libnccl.so.2), 1 = loopback. id: 128 bytes.

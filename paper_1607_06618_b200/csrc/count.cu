@@ -43,7 +43,8 @@ cudaError_t launch_inline(const CountArgs& a, int sms, cudaStream_t st) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_inline_kernel<W, TWO>, 128, 0);
   if (per_sm < 1) per_sm = 1;
-  const uint64_t chunks = (a.d1 - a.d0 + 31) / 32;
+  const uint32_t dpc = a.dpc ? a.dpc : 32u;
+  const uint64_t chunks = (a.d1 - a.d0 + dpc - 1) / dpc;
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (chunks + 3) / 4;
   if (grid > need) grid = need;

@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   RetryQueue& q = s_q[wib];
   uint32_t qn = 0;  // warp-uniform queue length
-  const uint64_t n_chunks = (a.d1 - a.d0 + 31) / 32;
+  const uint32_t dpc = a.dpc ? a.dpc : 32u;
+  const uint64_t n_chunks = (a.d1 - a.d0 + dpc - 1) / dpc;
   uint32_t first = 0, more = 0, maxp = 0;
 
   // Queue entries: key, bucket, probes | op << 24 — op 0 = look at the bucket,
@@ -197,8 +198,8 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
   };
   auto claimed = [&]() -> unsigned long long { return __shfl_sync(0xffffffffu, claim, 0); };
   auto desc_load = [&](unsigned long long chk) -> uint64_t {  // ~0 = no super-mer
-    const uint64_t di = a.d0 + chk * 32 + lane;
-    return (chk < n_chunks && di < a.d1) ? __ldg(a.desc + di) : ~0ull;
+    const uint64_t di = a.d0 + chk * dpc + lane;
+    return (chk < n_chunks && lane < dpc && di < a.d1) ? __ldg(a.desc + di) : ~0ull;
   };
   auto issue_words = [&](uint64_t d, uint64_t* dst) {  // one cp.async group per chunk
     uint32_t nwords = 0;

@@ -57,17 +57,18 @@ struct ProbeStats {
 template <int W, int WP, int U>
 __global__ void __launch_bounds__(kThreads) count_kernel(CountArgs a) {
   const uint32_t lane = lane_id();
-  const uint64_t n_chunks = (a.d1 - a.d0 + 31) / 32;
+  const uint32_t dpc = a.dpc ? a.dpc : 32u;
+  const uint64_t n_chunks = (a.d1 - a.d0 + dpc - 1) / dpc;
   ProbeStats ps;
   for (;;) {
     unsigned long long chk = 0;
     if (lane == 0) chk = atomicAdd(a.work, 1ull);
     chk = __shfl_sync(0xffffffffu, chk, 0);
     if (chk >= n_chunks) break;
-    const uint64_t di = a.d0 + chk * 32 + lane;
+    const uint64_t di = a.d0 + chk * dpc + lane;
     uint64_t pos = 0;
     uint32_t nw = 0;
-    if (di < a.d1) {
+    if (lane < dpc && di < a.d1) {
       const uint64_t d = __ldg(a.desc + di);
       pos = d >> kNwinBits;
       nw = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
@@ -233,7 +234,8 @@ cudaError_t launch_count_w(const CountArgs& a, int sms, cudaStream_t st) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, count_kernel<W, WP, U>, kThreads, 0);
   if (per_sm < 1) per_sm = 1;
-  const uint64_t chunks = (a.d1 - a.d0 + 31) / 32;
+  const uint32_t dpc = a.dpc ? a.dpc : 32u;
+  const uint64_t chunks = (a.d1 - a.d0 + dpc - 1) / dpc;
   uint64_t grid = (uint64_t)sms * per_sm;
   const uint64_t need = (chunks + kThreads / 32 - 1) / (kThreads / 32);
   if (grid > need) grid = need;

@@ -581,14 +581,11 @@ cudaError_t launch_plan_bins(const PlanBinsArgs& a, int sms, cudaStream_t st) {
 
 cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
+  if (key_words(a.k) >= 4) return launch_count_ref(a, sms, st);  // CTA-wide reference tables
   switch (key_words(a.k)) {
     case 1: return launch_smem<1, true>(a, sms, st);
     case 2: return smem_pack(a.k) ? launch_smem<2, true>(a, sms, st) : launch_smem<2, false>(a, sms, st);
     case 3: return launch_smem<3, false>(a, sms, st);
-    case 4: return launch_smem<4, false>(a, sms, st);
-    case 5: return launch_smem<5, false>(a, sms, st);
-    case 6: return launch_smem<6, false>(a, sms, st);
-    case 7: return launch_smem<7, false>(a, sms, st);
   }
   return cudaErrorInvalidValue;
 }

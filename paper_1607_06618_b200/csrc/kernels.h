@@ -122,6 +122,15 @@ struct GroupShuffleArgs {
 uint32_t group_shuffle_groups(uint32_t n_bins);
 size_t group_shuffle_scratch_bytes(uint32_t n_bins);
 cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_t s);
+// Multi-rank exchange of whole groups (shuffle.cu): per-group [3][G] windows / super-mers /
+// relocated payload words of bin-ordered descriptors (off = bin offsets), and the pack of every
+// group into the send buffers; base3 = [3][G]: first send descriptor, first send payload word,
+// and the first payload word in the OWNER's receive buffer of each group.
+cudaError_t launch_group_stats(const uint64_t* desc, const unsigned long long* off, uint32_t n_bins, uint32_t k,
+                               unsigned long long* st, cudaStream_t s);
+cudaError_t launch_group_pack(const uint64_t* desc, const unsigned long long* off, uint32_t n_bins,
+                              const uint64_t* codes, uint32_t k, const unsigned long long* base3, uint64_t* send_desc,
+                              uint32_t* send_bin, uint64_t* send_payload, cudaStream_t s);
 
 // world > 1: copy every local super-mer (descriptor + word-aligned payload)
 // into the send buffer, ordered by (destination rank, bin).
@@ -158,7 +167,15 @@ struct CountArgs {
   TableArgs t;
   unsigned long long* work;  // zeroed per launch: dynamic chunk counter
   uint32_t canonical;        // 1 = count min(x, rc x); 0 = `-d`
+  uint32_t dpc;              // descriptors per warp work unit (1..32; 0 = 32): fewer for long super-mers
 };
+// descriptors per work unit for super-mers of `avg_windows` windows on average: ~512 windows
+// per unit, at most 32 (one per lane)
+inline uint32_t count_dpc(double avg_windows) {
+  if (avg_windows <= 16.0) return 32;
+  const double d = 512.0 / avg_windows;
+  return d < 1.0 ? 1u : (uint32_t)d;
+}
 cudaError_t launch_count(const CountArgs& a, uint32_t W, int sms, cudaStream_t s);
 cudaError_t launch_count_wide(const CountArgs& a, int sms, cudaStream_t s);  // W = 8..15 (count_wide.cu)
 
@@ -203,7 +220,12 @@ int smem_count_warps(uint32_t k);                            // warps per CTA (G
 uint32_t smem_slot_bytes(uint32_t k);
 uint32_t smem_warp_bytes(uint32_t k, uint32_t cap);
 uint32_t smem_table_slots(uint32_t k, size_t smem_per_block, int warps = 0);  // 0 = no room
-cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);  // W >= 4: count_ref
+// count_ref.cu (W >= 4): a.cap = slots of the CTA-wide table of occurrence references
+size_t ref_table_bytes(uint32_t cap);
+uint32_t ref_table_slots(size_t smem_per_block);
+uint32_t ref_max_fill(uint32_t cap);
+cudaError_t launch_count_ref(const SmemCountArgs& a, int sms, cudaStream_t s);
 struct PlanBinsArgs {
   const unsigned long long* win;   // [n_bins] windows per bin (step b histogram)
   const unsigned long long* off;   // [n_bins + 1] first descriptor of each bin (exclusive scan)

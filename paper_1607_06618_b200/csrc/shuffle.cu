@@ -422,7 +422,131 @@ __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t*
   }
 }
 
+// ---- multi-rank exchange of whole groups (a group = 1024 consecutive bins) ----------------
+// group_stats: per group g of the bin-ordered descriptors: windows, super-mers and the payload
+// words its super-mers take once relocated (ceil((nwin + k - 1) / 32) each), laid out
+// [3][G] like the histograms of exchange_plan.
+__global__ void __launch_bounds__(256) group_stats_kernel(const uint64_t* __restrict__ desc,
+                                                          const unsigned long long* __restrict__ off,
+                                                          uint32_t n_bins, uint32_t k, unsigned long long* st) {
+  const uint32_t g = blockIdx.x, G = gridDim.x;
+  const uint32_t b0 = g << kGroupShift, b1 = min(b0 + (1u << kGroupShift), n_bins);
+  const unsigned long long i0 = off[b0], i1 = off[b1];
+  unsigned long long w = 0, pw = 0;
+  for (unsigned long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const uint32_t nw = (uint32_t)(__ldg(desc + i) & ((1u << kNwinBits) - 1)) + 1;
+    w += nw;
+    pw += (nw + k - 1 + 31) / 32;
+  }
+  __shared__ unsigned long long s_w[8], s_p[8];
+  for (int o = 16; o > 0; o >>= 1) {
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+    pw += __shfl_xor_sync(0xffffffffu, pw, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_w[threadIdx.x >> 5] = w;
+    s_p[threadIdx.x >> 5] = pw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tw = 0, tp = 0;
+    for (int q = 0; q < 8; ++q) {
+      tw += s_w[q];
+      tp += s_p[q];
+    }
+    st[g] = tw;
+    st[G + g] = i1 - i0;
+    st[2 * G + g] = tp;
+  }
+}
+
+// group_pack: one CTA per group copies the group's super-mers into the send buffers at the
+// group's place in its owner's segment: descriptor (position rebased to the owner's receive
+// payload buffer: abs_word[g] words plus the super-mer's offset inside the group), its bin,
+// and the payload (bases [pos, pos + nwin + k - 1) re-aligned to word boundaries).
+__global__ void __launch_bounds__(256) group_pack_kernel(const uint64_t* __restrict__ desc,
+                                                         const unsigned long long* __restrict__ off,
+                                                         uint32_t n_bins, const uint64_t* __restrict__ codes,
+                                                         uint32_t k, const unsigned long long* __restrict__ base3,
+                                                         uint64_t* __restrict__ send_desc,
+                                                         uint32_t* __restrict__ send_bin,
+                                                         uint64_t* __restrict__ send_payload) {
+  constexpr uint32_t kFan = 1u << kGroupShift;
+  __shared__ unsigned long long s_off[kFan + 1];
+  __shared__ uint32_t s_wsum[8];
+  const uint32_t g = blockIdx.x, G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t b0 = g << kGroupShift, nb = min(kFan, n_bins - b0);
+  for (uint32_t t = tid; t <= nb; t += blockDim.x) s_off[t] = off[b0 + t];
+  __syncthreads();
+  const unsigned long long i0 = s_off[0], i1 = s_off[nb];
+  const unsigned long long dbase = base3[g], wbase = base3[G + g], abase = base3[2 * G + g];
+  unsigned long long run = 0;  // payload words of the group's earlier super-mers
+  for (unsigned long long c0 = i0; c0 < i1; c0 += blockDim.x) {
+    const unsigned long long i = c0 + tid;
+    uint64_t d = 0;
+    uint32_t nw = 0, wds = 0;
+    if (i < i1) {
+      d = __ldg(desc + i);
+      nw = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
+      wds = (nw + k - 1 + 31) / 32;
+    }
+    uint32_t incl = wds;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wex = 0, tot = 0;
+    for (uint32_t q = 0; q < blockDim.x / 32; ++q) {
+      if (q < warp) wex += s_wsum[q];
+      tot += s_wsum[q];
+    }
+    const unsigned long long woff = run + wex + incl - wds;
+    if (i < i1) {
+      // bin: the last f with s_off[f] <= i (bins of the group are consecutive ranges)
+      uint32_t f = 0;
+      for (uint32_t step = kFan >> 1; step >= 1; step >>= 1)
+        if (f + step < nb && s_off[f + step] <= i) f += step;
+      const uint64_t pos = d >> kNwinBits, L = nw + k - 1;
+      uint64_t* dst = send_payload + wbase + woff;
+      for (uint32_t u = 0; u < wds; ++u) {
+        const uint64_t q = pos + 32ull * u;
+        const uint64_t e = (q + 32 < pos + L) ? q + 32 : pos + L;  // bases [q, e)
+        const uint64_t w0 = q >> 5;
+        const uint32_t sh = (uint32_t)(q & 31) * 2;
+        const uint64_t hi = __ldg(codes + w0);
+        const uint64_t lo = (((e - 1) >> 5) > w0) ? __ldg(codes + w0 + 1) : 0ull;
+        uint64_t v = sh ? ((hi << sh) | (lo >> (64 - sh))) : hi;
+        const uint32_t nbs = (uint32_t)(e - q);
+        if (nbs < 32) v &= ~0ull << (64 - 2 * nbs);
+        dst[u] = v;
+      }
+      const unsigned long long j = dbase + (i - i0);
+      send_desc[j] = (((abase + woff) * 32ull) << kNwinBits) | (nw - 1);
+      send_bin[j] = b0 + f;
+    }
+    run += tot;
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_group_stats(const uint64_t* desc, const unsigned long long* off, uint32_t n_bins, uint32_t k,
+                               unsigned long long* st, cudaStream_t s) {
+  const uint32_t G = ((n_bins - 1) >> kGroupShift) + 1;
+  group_stats_kernel<<<G, 256, 0, s>>>(desc, off, n_bins, k, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_pack(const uint64_t* desc, const unsigned long long* off, uint32_t n_bins,
+                              const uint64_t* codes, uint32_t k, const unsigned long long* base3, uint64_t* send_desc,
+                              uint32_t* send_bin, uint64_t* send_payload, cudaStream_t s) {
+  const uint32_t G = ((n_bins - 1) >> kGroupShift) + 1;
+  group_pack_kernel<<<G, 256, 0, s>>>(desc, off, n_bins, codes, k, base3, send_desc, send_bin, send_payload);
+  return cudaGetLastError();
+}
 
 uint32_t group_shuffle_groups(uint32_t n_bins) { return ((n_bins - 1) >> kGroupShift) + 1; }
 

@@ -55,8 +55,10 @@ CONFIGS = {
     "C3k65": Config("C3k65", "H. sapiens-scale synthetic reads (per-GPU shard of 100 Gbp / 8)", 4, 3_100_000_000,
                     100, 125_000_000, 0.0021, 0.0001, 65, 15, 1),
     "C3k100": Config("C3k100", "H. sapiens-scale synthetic reads (per-GPU shard of 100 Gbp / 8)", 4, 3_100_000_000,
-                     100, 125_000_000, 0.0021, 0.0001, 100, 7, 1),
-    # configs[4]: long reads 1e7 x 10 kbp over 8 GPUs, 1 % error, k = 200, min_count = 2 (m = 11, 4096 bins: SURVEY §8(d))
+                     100, 125_000_000, 0.0021, 0.0001, 100, 15, 1),
+    # configs[4]: long reads 1e7 x 10 kbp over 8 GPUs, 1 % error, k = 200, min_count = 2. m = 15 (reading Q25,
+    # results invariant in m; SURVEY §8(d) proposed m = 11, whose few popular minimizers leave most windows in
+    # bins too large for a table), bins: the library's auto policy (~2^21 for count_ref.cu's reference tables)
     "C4": Config("C4", "synthetic long reads, 10 kbp, 1% error (per-GPU shard of 100 Gbp / 8)", 5, 3_100_000_000,
-                 10_000, 1_250_000, 0.01, 0.0, 200, 11, 2, n_bins=4096),
+                 10_000, 1_250_000, 0.01, 0.0, 200, 15, 2),
 }

@@ -320,6 +320,19 @@ def test_forced_exchange_single_rank(G, backend):
         assert st["count_sum"] == ref.windows
 
 
+@pytest.mark.parametrize("backend", [0, 1])
+def test_forced_group_exchange_single_rank(G, backend):
+    # world = 1, exchange forced, 2^16 bins: the group exchange path (NCCL to self / loopback)
+    w = synth.Workload(seed=44, genome_len=30_000, read_len=150, n_reads=4000, err=0.004, nrate=0.001)
+    text = synth.fastx(w, synth.FASTQ)
+    for k in (40, 65, 130):
+        ref = oracle.count(text, k)
+        keys, counts, st = _gpu_count_text(G, text, k, 15, 1, force_exchange=True, comm_backend=backend,
+                                           n_bins=1 << 16)
+        compare(keys, counts, k, ref)
+        assert st["count_sum"] == ref.windows and st["smem_windows"] > 0
+
+
 # ---- multi-rank shard logic: loopback group (P virtual ranks on one GPU) ---------------
 @pytest.mark.parametrize("P", [2, 3, 4])
 def test_loopback_ranks_parity(G, P):
@@ -406,3 +419,68 @@ def test_parity_compressed_files(G, codec, tmp_path):
         st = g.stats()
     compare(keys, counts, 40, ref)
     assert st["count_sum"] == ref.windows
+
+
+# ---- world > 1 with the device bin plan: whole groups of 1024 bins exchanged ----------------
+@pytest.mark.parametrize("P,k", [(2, 40), (4, 40), (3, 65), (2, 150), (4, 201)])
+def test_loopback_group_exchange(G, P, k):
+    # 2^16 bins (the device plan): every rank groups its super-mers, the per-group histograms are
+    # all-gathered, whole groups go to their LPT owner in one grouped all-to-all (descriptors,
+    # bins, payload), and each owner counts its groups with the shared-memory / reference tables
+    w = synth.Workload(seed=90 + k, genome_len=60_000, read_len=250, n_reads=3000, err=0.006, nrate=0.001)
+    ref = oracle.count(synth.fastx(w, synth.FASTQ), k)
+    uid = bytes([P + 16 * (k % 7)]) * 128
+    results = [None] * P
+    errors = []
+
+    def rank(r):
+        try:
+            with G.Gerbil(rank=r, world=P, unique_id=uid, comm_backend=1, n_bins=1 << 16) as g:
+                g.count(k, 15, 1, text=synth.fastx(w.shard(r, P), synth.FASTQ))
+                results[r] = g.fetch(sorted=True) + (g.stats(),)
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    keys = np.concatenate([r[0] for r in results])
+    counts = np.concatenate([r[1] for r in results])
+    strs = decode_keys(keys, k)
+    order = sorted(range(len(strs)), key=lambda i: strs[i])
+    compare(keys[order], counts[order], k, ref)
+    assert sum(r[2]["count_sum"] for r in results) == ref.windows
+    assert all(r[2]["smem_windows"] > 0 and r[2]["bytes_recv"] > 0 for r in results)
+
+
+def test_loopback_auto_bins_agree(G):
+    # n_bins = 0 (auto) with world > 1: the ranks derive B from the all-gathered totals
+    P, k = 2, 40
+    w = synth.Workload(seed=5, genome_len=40_000, read_len=120, n_reads=4000, err=0.004)
+    ref = oracle.count(synth.fastx(w, synth.FASTQ), k)
+    uid = b"\x7f" * 128
+    results, errors = [None] * P, []
+
+    def rank(r):
+        try:
+            with G.Gerbil(rank=r, world=P, unique_id=uid, comm_backend=1) as g:
+                g.count(k, 15, 1, text=synth.fastx(w.shard(r, P), synth.FASTQ))
+                results[r] = g.fetch(sorted=True) + (g.stats(),)
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert results[0][2]["n_bins"] == results[1][2]["n_bins"]
+    keys = np.concatenate([r[0] for r in results])
+    counts = np.concatenate([r[1] for r in results])
+    strs = decode_keys(keys, k)
+    order = sorted(range(len(strs)), key=lambda i: strs[i])
+    compare(keys[order], counts[order], k, ref)

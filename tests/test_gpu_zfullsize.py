@@ -16,8 +16,11 @@ Cases (synth/configs.py holds the workloads bench.py runs):
   * C1 at m=7 (auto bins → L2 wave tables only).
   * C3k65 (`bench.py --config C3k65` launch configuration: k=65, W=3 keys, m=15,
     auto bins) on a 2.5 Gbp prefix of the shard.
-  * C4 (`bench.py --config C4`: 10-kbp reads, 1 % error, k=200, m=11, 4096
-    bins, min_count=2) on a 2.5 Gbp prefix of the shard.
+  * C3k100 (`bench.py --config C3k100`: k=100, W=4 keys, one window per read,
+    m=15, auto bins → the reference tables of count_ref.cu) on a 2.5 Gbp prefix.
+  * C4 (`bench.py --config C4`: 10-kbp reads, 1 % error, k=200, m=11, auto bins
+    → reference tables, min_count=2) on a 2.5 Gbp prefix of the shard; the test
+    asserts that the reference tables counted most windows.
 GERBIL_FULLSIZE_SCALE (float, default 1) scales every case's read count.
 """
 import os
@@ -39,7 +42,8 @@ CASES = [
     ("C1-bench", "C1", None, None, "bench"),
     ("C1-m7", "C1", 7, None, ""),
     ("C3k65", "C3k65", None, 25_000_000, ""),
-    ("C4", "C4", None, 250_000, ""),
+    ("C3k100", "C3k100", None, 25_000_000, "ref"),
+    ("C4", "C4", None, 250_000, "ref"),
 ]
 
 
@@ -93,6 +97,8 @@ def test_fullsize_sampled_parity(case):
         assert st["smem_windows"] > 0.95 * st["valid_windows"], st
         assert st["smem_failed"] > 0, st
         assert st["waves"] >= 1, st
+    if check == "ref":  # the long-k reference tables (count_ref.cu) counted the bulk
+        assert st["smem_windows"] > 0.9 * st["valid_windows"], st
     keep = _fnv_keep(keys, cfg.k, SAMPLE)
     sk, sc = keys[keep], counts[keep]
     del keys, counts
