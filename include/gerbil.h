@@ -254,6 +254,18 @@ gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted,
 /* Same, written to a file (GERBIL_E_IO if it cannot be written). */
 gerbil_status gerbil_write_results(gerbil_ctx* ctx, const char* path, int32_t format, int sorted);
 
+/* Host-only k-way merge of n_lists SORTED result lists — e.g. the sorted fetches of the
+ * ranks of one job, whose key sets are disjoint (every bin has one owner) —
+ * into one list in ascending key order (SURVEY.md §3.4 "cross-GPU merge").
+ * keys[l] holds n[l] * W words, counts[l] n[l] counts (caller-owned, unchanged). Keys present
+ * in several lists are merged into one entry with the summed count (merging histograms of
+ * independent jobs). out_keys == NULL → only *n_out (the merged entry count) is written;
+ * otherwise out_keys[*n_out * W] / out_counts[*n_out] receive the list (capacity = entries).
+ * threads <= 0 = all host cores. GERBIL_E_USAGE on bad arguments or a too small capacity. */
+gerbil_status gerbil_merge_sorted(uint32_t n_lists, const uint64_t* const* keys, const uint32_t* const* counts,
+                                  const uint64_t* n, uint32_t W, int32_t threads, uint64_t* out_keys,
+                                  uint32_t* out_counts, uint64_t capacity, uint64_t* n_out);
+
 /* ---- step (a) on the device --------------------
  * "Phase one on the GPU" (the paper's future work): a FASTA /
  * FASTQ / raw document (App. B) is parsed by kernels into the

@@ -227,6 +227,7 @@ struct gerbil_ctx {
   int smem_optin = 0;  // max dynamic shared memory per block (bytes)
   PinnedBuf h_hist, h_rng;  // per-bin histogram download, shared-memory bin list upload
   DevBuf bin_off_d, plan_sums;  // device-side bin plan (many bins, one rank)
+  bool results_sorted = false;   // out_keys already in A<C<G<T order (a sorted fetch ran)
   Counters* h_counters = nullptr;  // pinned
   // results
   bool have_result = false;
@@ -1426,6 +1427,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
                                 uint32_t min_count, bool fresh = true) {
   const double t0 = wall_ms();
   ctx->have_result = false;
+  ctx->results_sorted = false;
   ctx->n_out = 0;
   if (fresh) begin_call(ctx);
   memset(&ctx->stats, 0, sizeof ctx->stats);
@@ -2435,10 +2437,26 @@ gerbil_status gerbil_fetch(gerbil_ctx* ctx, uint64_t* kmers, uint32_t* counts, u
   if (capacity < ctx->n_out) return fail(ctx, GERBIL_E_USAGE, "capacity too small");
   const uint64_t n = ctx->n_out, W = ctx->W;
   CK(cudaSetDevice(ctx->device));
+  bool host_sort = false;
+  if (sorted && n > 1 && !ctx->results_sorted) {
+    // device LSD radix sort (sort.cu) of the results in place; only if its temporaries do not
+    // fit does the host sort them after the copy
+    DevBuf tk, tc, sc;
+    if (tk.ensure(n * W * 8) == cudaSuccess && tc.ensure(n * 4) == cudaSuccess &&
+        sc.ensure(sort_scratch_words(n) * 8) == cudaSuccess) {
+      CK(launch_sort_results(ctx->out_keys.as<uint64_t>(), ctx->out_counts.as<uint32_t>(), n, (uint32_t)W, ctx->k,
+                             tk.as<uint64_t>(), tc.as<uint32_t>(), sc.as<uint64_t>(), ctx->sms, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->results_sorted = true;
+    } else {
+      cudaGetLastError();
+      host_sort = true;
+    }
+  }
   CK(cudaMemcpyAsync(kmers, ctx->out_keys.p, n * W * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (counts) CK(cudaMemcpyAsync(counts, ctx->out_counts.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  if (sorted && n > 1) {
+  if (host_sort) {
     std::vector<uint64_t> idx(n);
     std::iota(idx.begin(), idx.end(), 0ull);
     std::sort(idx.begin(), idx.end(), [&](uint64_t a, uint64_t b) {
@@ -2472,6 +2490,20 @@ gerbil_status gerbil_encode_results(gerbil_ctx* ctx, int32_t format, int sorted,
   if (!out) return GERBIL_OK;
   if (capacity < need) return fail(ctx, GERBIL_E_USAGE, "capacity too small");
   encode_results(format, keys.data(), counts.data(), got, ctx->k, (uint32_t)W, out, ctx->cfg.host_threads);
+  return GERBIL_OK;
+}
+
+gerbil_status gerbil_merge_sorted(uint32_t n_lists, const uint64_t* const* keys, const uint32_t* const* counts,
+                                  const uint64_t* n, uint32_t W, int32_t threads, uint64_t* out_keys,
+                                  uint32_t* out_counts, uint64_t capacity, uint64_t* n_out) {
+  if (!n_out || W == 0 || W > (uint32_t)kMaxW || (n_lists && (!keys || !counts || !n))) return GERBIL_E_USAGE;
+  for (uint32_t l = 0; l < n_lists; ++l)
+    if (n[l] && (!keys[l] || !counts[l])) return GERBIL_E_USAGE;
+  const uint64_t m = merge_sorted(n_lists, keys, counts, n, W, nullptr, nullptr, threads);
+  *n_out = m;
+  if (!out_keys) return GERBIL_OK;
+  if (!out_counts || capacity < m) return GERBIL_E_USAGE;
+  merge_sorted(n_lists, keys, counts, n, W, out_keys, out_counts, threads);
   return GERBIL_OK;
 }
 

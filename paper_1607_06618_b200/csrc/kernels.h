@@ -275,4 +275,9 @@ cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t s);
 
 cudaError_t launch_clear_table(unsigned char* table, uint64_t bytes, int sms, cudaStream_t s);
 
+// sort.cu: LSD radix sort of n results (W-word keys of k bases, u32 counts) into A<C<G<T order
+uint64_t sort_scratch_words(uint64_t n);
+cudaError_t launch_sort_results(uint64_t* keys, uint32_t* cnt, uint64_t n, uint32_t W, uint32_t k, uint64_t* keys_tmp,
+                                uint32_t* cnt_tmp, uint64_t* scratch, int sms, cudaStream_t s);
+
 }  // namespace gerbil

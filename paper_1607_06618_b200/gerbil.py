@@ -132,6 +132,7 @@ _lib.gerbil_count_host_stream.argtypes = [_P, _P, _P, _P, C.c_uint64, C.c_uint32
                                           C.c_uint64, _U64P]
 _lib.gerbil_pack_reads.argtypes = [C.POINTER(Reads), C.c_int32, _P, _P, _P, _U64P, _U64P, C.c_char_p, C.c_size_t]
 _lib.gerbil_fetch.argtypes = [_P, _P, _P, C.c_uint64, _U64P, C.c_int]
+_lib.gerbil_merge_sorted.argtypes = [C.c_uint32, _P, _P, _P, C.c_uint32, C.c_int32, _P, _P, C.c_uint64, _U64P]
 _lib.gerbil_results_device.argtypes = [_P, C.POINTER(_P), C.POINTER(_P), _U64P, C.POINTER(C.c_uint32)]
 _lib.gerbil_get_stats.argtypes = [_P, C.POINTER(Stats)]
 _lib.gerbil_last_error.argtypes = [_P]
@@ -156,6 +157,7 @@ EXPORTED = [
     "gerbil_parse_text", "gerbil_count_text",
     "gerbil_results_device", "gerbil_get_stats", "gerbil_last_error", "gerbil_finalize",
     "gerbil_debug_supermers", "gerbil_encode_results", "gerbil_write_results", "gerbil_exchange_plan",
+    "gerbil_merge_sorted",
 ]
 
 
@@ -204,6 +206,29 @@ def exchange_plan(hist: np.ndarray, rank: int) -> ExchangePlan:
     if st != OK:
         raise GerbilError(st, "gerbil_exchange_plan failed")
     return ExchangePlan(owner, *offs)
+
+
+def merge_sorted(lists: list[tuple[np.ndarray, np.ndarray]], threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """k-way merge (host, gerbil_merge_sorted) of sorted (keys[n, W] u64, counts[n] u32) lists —
+    e.g. the sorted fetches of every rank — into one sorted list; equal keys sum their counts."""
+    W = next((int(k.shape[1]) for k, _ in lists if k.ndim == 2), 1)
+    ks = [np.ascontiguousarray(k, dtype=np.uint64).reshape(-1, W) for k, _ in lists]
+    cs = [np.ascontiguousarray(c, dtype=np.uint32) for _, c in lists]
+    kp = (C.c_void_p * max(len(ks), 1))(*[k.ctypes.data for k in ks])
+    cp = (C.c_void_p * max(len(cs), 1))(*[c.ctypes.data for c in cs])
+    n = np.array([k.shape[0] for k in ks], np.uint64)
+    m = C.c_uint64()
+    st = _lib.gerbil_merge_sorted(len(ks), C.cast(kp, C.c_void_p), C.cast(cp, C.c_void_p), _ptr(n), W, threads,
+                                  None, None, 0, C.byref(m))
+    if st != OK:
+        raise GerbilError(st, "gerbil_merge_sorted failed")
+    ok = np.zeros((m.value, W), np.uint64)
+    oc = np.zeros(m.value, np.uint32)
+    st = _lib.gerbil_merge_sorted(len(ks), C.cast(kp, C.c_void_p), C.cast(cp, C.c_void_p), _ptr(n), W, threads,
+                                  _ptr(ok), _ptr(oc), m.value, C.byref(m))
+    if st != OK:
+        raise GerbilError(st, "gerbil_merge_sorted failed")
+    return ok, oc
 
 
 @dataclass

@@ -484,3 +484,25 @@ def test_loopback_auto_bins_agree(G):
     strs = decode_keys(keys, k)
     order = sorted(range(len(strs)), key=lambda i: strs[i])
     compare(keys[order], counts[order], k, ref)
+
+
+# ---- sorted fetch: device LSD radix sort (sort.cu) ------------------------------------------
+@pytest.mark.parametrize("k,read_len", [(28, 150), (40, 150), (100, 300), (479, 700)])
+def test_device_sorted_fetch_matches_lexsort(G, k, read_len):
+    # the sorted fetch (device radix sort over the 2k meaningful bits) equals numpy's lexicographic
+    # sort of the unsorted fetch, for ~10^6 results (hundreds of tiles, ragged tail)
+    w = synth.Workload(seed=k, genome_len=2_000_000, read_len=read_len, n_reads=max(2000, 3_000_000 // read_len),
+                       err=0.01)
+    codes, nmask, rs = synth.packed_device(w)
+    import torch
+
+    torch.cuda.synchronize()
+    with G.Gerbil() as g:
+        g.count_device(codes, nmask, rs, w.n_reads, k, 15, 1)
+        uk, uc = g.fetch(sorted=False)
+        sk, sc = g.fetch(sorted=True)
+        sk2, sc2 = g.fetch(sorted=False)  # stays sorted on the device
+    assert uk.shape[0] > 100_000
+    order = np.lexsort(tuple(uk[:, j] for j in reversed(range(uk.shape[1]))))
+    assert np.array_equal(sk, uk[order]) and np.array_equal(sc, uc[order])
+    assert np.array_equal(sk2, sk) and np.array_equal(sc2, sc)

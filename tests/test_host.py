@@ -165,3 +165,29 @@ def test_reader_compressed_inputs(tmp_path):
         with pytest.raises(gerbil.GerbilError) as e:
             gerbil.pack_reads(paths=[str(f)])
         assert name in str(e.value)
+
+
+@pytest.mark.parametrize("W,threads", [(1, 1), (2, 4), (7, 3)])
+def test_merge_sorted_lists(W, threads):
+    # host k-way merge of per-rank sorted results: disjoint key sets interleave
+    # into one sorted list; a key in several lists sums its counts; empty lists are fine
+    from paper_1607_06618_b200 import gerbil
+
+    rng = np.random.default_rng(W)
+    n_total = 200_000
+    keys = np.unique(rng.integers(0, 2**63, size=(n_total, W), dtype=np.uint64), axis=0)
+    counts = rng.integers(1, 1000, size=keys.shape[0]).astype(np.uint32)
+    owner = rng.integers(0, 4, size=keys.shape[0])
+    lists = [(keys[owner == r], counts[owner == r]) for r in range(4)] + [(np.zeros((0, W), np.uint64),
+                                                                          np.zeros(0, np.uint32))]
+    mk, mc = gerbil.merge_sorted(lists, threads=threads)
+    assert np.array_equal(mk, keys) and np.array_equal(mc, counts)
+    # overlapping lists (two independent jobs): union with summed counts
+    a = (keys[::2], counts[::2])
+    b = (keys[::3], counts[::3])
+    mk, mc = gerbil.merge_sorted([a, b], threads=threads)
+    idx2, idx3 = set(range(0, keys.shape[0], 2)), set(range(0, keys.shape[0], 3))
+    both = sorted(idx2 | idx3)
+    assert np.array_equal(mk, keys[both])
+    exp = np.array([(counts[i] if i in idx2 else 0) + (counts[i] if i in idx3 else 0) for i in both], np.uint32)
+    assert np.array_equal(mc, exp)
