@@ -28,7 +28,7 @@ NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-rela
 EXTRA = os.environ.get("GERBIL_NVCC_EXTRA", "").split()
 NVFLAGS += EXTRA
 
-GERBIL_CU = ["parse.cu", "supermer.cu", "supermer_reads.cu", "ordering.cu", "shuffle.cu", "count.cu", "count_wide.cu", "count_smem.cu", "count_ref.cu", "sort.cu", "compact.cu", "comm.cu",
+GERBIL_CU = ["parse.cu", "supermer.cu", "supermer_reads.cu", "ordering.cu", "shuffle.cu", "count.cu", "count_wide.cu", "count_smem.cu", "count_ref.cu", "sort.cu", "compact.cu", "comm.cu", "waves.cu", "pipeline.cu", "io.cu", "spill.cu", "results.cu",
              "api.cu"]
 GERBIL_CPP = ["reader.cpp", "output.cpp"]
 
