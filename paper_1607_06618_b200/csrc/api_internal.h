@@ -215,13 +215,15 @@ struct gerbil_ctx {
   DevBuf hist_all, cursor, cursor2, seg_base;
   DevBuf table, ovf, out_keys, out_counts, wave_distinct;
   DevBuf rec_stage, rec_meta;
+  DevBuf rec_stage2, rec_snap_d;  // streaming call, shared-memory pass: record staging, result snapshots
   DevBuf order_rank, order_freq;  // DFP ordering: key table [4^m] and its sample histogram
   DevBuf text_buf, p_cnt, p_off, p_ls, p_cr, p_eff, p_first, p_seq, p_rflag, p_pos, p_ridx, p_tmp, p_misc;  // parser
   uint32_t m = 0;  // streaming call: per-lane record staging; counters/snapshots/offsets
   DevBuf send_desc, send_bin, send_payload, recv_desc, recv_bin, recv_payload;
   DevBuf smem_range, smem_failed, rest_desc, rest_range, rest_off;  // step (d) in shared memory
   int smem_optin = 0;  // max dynamic shared memory per block (bytes)
-  PinnedBuf h_hist, h_rng;  // per-bin histogram download, shared-memory bin list upload
+  size_t mem_total = 0;  // device memory (bytes), read once
+  PinnedBuf h_hist, h_rng, h_fail;  // per-bin histogram download, bin list upload, abandoned bins
   DevBuf bin_off_d, plan_sums;  // device-side bin plan (many bins, one rank)
   bool results_sorted = false;   // out_keys already in A<C<G<T order (a sorted fetch ran)
   Counters* h_counters = nullptr;  // pinned
@@ -341,7 +343,7 @@ inline uint32_t choose_bins(gerbil_ctx* ctx, uint64_t n_bases, uint64_t n_reads,
     const double len = (double)n_bases / (double)n_reads;
     windows = std::min(windows, (double)n_reads * std::max(0.0, len - (double)k + 1.0));
   }
-  const uint32_t cap = (ctx->rec_out || m < 11) ? 0u : smem_slots_for(ctx, k);
+  const uint32_t cap = m < 11 ? 0u : smem_slots_for(ctx, k);
   if (cap) {
     const double want = ctx->rho * windows / (0.35 * cap);
     uint32_t B = 512;
@@ -405,6 +407,32 @@ inline void exchange_plan(const uint64_t* H, uint32_t B, int P, int r, int32_t* 
   }
 }
 
+// Small device → page-locked host read on ctx->stream. During a streaming call the copy engine
+// is busy with the record copies (GB), behind which a cudaMemcpy would queue: a kernel writes the
+// words through the mapping instead.
+inline cudaError_t d2h_small(gerbil_ctx* ctx, void* host_pinned, const void* dev, size_t bytes) {
+  if (!ctx->rec_out) return cudaMemcpyAsync(host_pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+  unsigned long long* mapped = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer((void**)&mapped, host_pinned, 0);
+  if (e != cudaSuccess) return e;
+  return launch_copy_words_mapped(mapped, reinterpret_cast<const unsigned long long*>(dev), (bytes + 7) / 8,
+                                  ctx->stream);
+}
+
+// results (W key words + u32 count) a fixed 1/div share of the device memory holds (>= 1)
+inline uint64_t result_budget_entries(gerbil_ctx* ctx, uint32_t W, uint32_t div) {
+  if (!ctx->mem_total) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      tot = 64ull << 30;
+    }
+    ctx->mem_total = tot;
+  }
+  const uint64_t n = (uint64_t)(ctx->mem_total / div) / (W * 8ull + 4ull);
+  return n ? n : 1;
+}
+
 inline double wall_ms() {
   return std::chrono::duration<double, std::milli>(
              std::chrono::steady_clock::now().time_since_epoch())
@@ -448,7 +476,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
                           const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
                           uint64_t total_windows);
 gerbil_status group_shuffle(gerbil_ctx* ctx, const uint64_t* desc_in, const uint32_t* bin_in, uint64_t n, uint32_t B,
-                            uint64_t* tmp_desc, uint32_t* tmp_bin, uint64_t* desc_alt);
+                            uint64_t* tmp_desc, uint32_t* tmp_bin, uint64_t* desc_alt, uint64_t max_windows);
 gerbil_status exchange_groups(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B, uint32_t cap,
                               uint32_t k, uint32_t min_count, uint64_t& owned_windows);
 gerbil_status build_dfp_table(gerbil_ctx* ctx, const SupermerArgs& a, uint64_t n_bases, uint32_t m);

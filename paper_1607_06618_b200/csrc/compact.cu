@@ -296,7 +296,106 @@ __global__ void __launch_bounds__(kThreads) compact_inline_kernel(CompactArgs a)
   }
 }
 
+// App. C records of results [*lo, *hi) of a result array (shared-memory / reference passes
+// write (key, count) arrays; the streaming call turns each slice of them into records here):
+// per CTA iteration the records are sized, block-scanned, reserved with one atomic on
+// *rec_n and written through shared memory with aligned 16-byte stores (flush_records).
+__global__ void __launch_bounds__(kThreads) encode_records_kernel(const uint64_t* __restrict__ keys,
+                                                                  const uint32_t* __restrict__ counts,
+                                                                  const unsigned long long* lo,
+                                                                  const unsigned long long* hi, uint32_t k,
+                                                                  uint8_t* rec, uint64_t rec_cap,
+                                                                  unsigned long long* rec_n) {
+  __shared__ uint32_t s_w[kWarps];
+  __shared__ unsigned long long s_rbase;
+  __shared__ uint32_t s_rtot;
+  extern __shared__ __align__(16) uint8_t s_rec[];  // [16 + kThreads * kPer * (5 + kb)]
+  const uint32_t kb = (k + 3) / 4, W = key_words(k);
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const unsigned long long e0 = *lo, e1 = *hi;
+  for (unsigned long long base = e0 + (uint64_t)blockIdx.x * kThreads * kPer; base < e1;
+       base += (uint64_t)gridDim.x * kThreads * kPer) {
+    // thread tid owns entries base + tid*kPer .. +kPer (contiguous: one scan value per thread)
+    uint32_t sz = 0, cnt[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const unsigned long long e = base + (uint64_t)tid * kPer + j;
+      cnt[j] = e < e1 ? counts[e] : 0u;
+      if (e < e1) sz += record_bytes(kb, cnt[j]);
+    }
+    uint32_t incl = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t v = s_w[w];
+        s_w[w] = run;
+        run += v;
+      }
+      s_rtot = run;
+      s_rbase = run ? atomicAdd(rec_n, (unsigned long long)run) : 0ull;
+    }
+    __syncthreads();
+    uint32_t o = (uint32_t)(s_rbase & 15) + s_w[warp] + incl - sz;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const unsigned long long e = base + (uint64_t)tid * kPer + j;
+      if (e < e1) {
+        put_record(s_rec, o, keys + e * W, kb, cnt[j]);
+        o += record_bytes(kb, cnt[j]);
+      }
+    }
+    __syncthreads();
+    flush_records(s_rec, s_rtot, s_rbase, rec, rec_cap);
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+// *dst = *src, dst in page-locked (mapped) host memory: a counter snapshot that does not queue
+// behind the large record copies on the copy engine
+__global__ void store_u64_kernel(unsigned long long* dst, const unsigned long long* src) {
+  *reinterpret_cast<volatile unsigned long long*>(dst) = *reinterpret_cast<const volatile unsigned long long*>(src);
+  __threadfence_system();
+}
+cudaError_t launch_store_u64(unsigned long long* dst_mapped, const unsigned long long* src, cudaStream_t st) {
+  store_u64_kernel<<<1, 1, 0, st>>>(dst_mapped, src);
+  return cudaGetLastError();
+}
+
+__global__ void copy_words_kernel(unsigned long long* dst, const unsigned long long* src, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<volatile unsigned long long*>(dst)[i] = src[i];
+  __threadfence_system();
+}
+cudaError_t launch_copy_words_mapped(unsigned long long* dst_mapped, const unsigned long long* src, uint64_t n,
+                                     cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t g = (n + 255) / 256;
+  copy_words_kernel<<<(unsigned)(g < 64 ? g : 64), 256, 0, st>>>(dst_mapped, src, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_encode_records(const uint64_t* keys, const uint32_t* counts, const unsigned long long* lo,
+                                  const unsigned long long* hi, uint64_t max_n, uint32_t k, uint8_t* rec,
+                                  uint64_t rec_cap, unsigned long long* rec_n, int sms, cudaStream_t st) {
+  if (max_n == 0) return cudaSuccess;
+  const uint32_t rec_max = 5 + (k + 3) / 4;
+  const size_t dyn = 16 + (size_t)kThreads * kPer * rec_max;
+  cudaError_t e = cudaFuncSetAttribute(encode_records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  if (e != cudaSuccess) return e;
+  uint64_t grid = (max_n + kThreads * kPer - 1) / (kThreads * kPer);
+  if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+  encode_records_kernel<<<(unsigned)grid, kThreads, dyn, st>>>(keys, counts, lo, hi, k, rec, rec_cap, rec_n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t st) {
   const uint64_t n_slots = a.nb * kSlotsPerBucket;

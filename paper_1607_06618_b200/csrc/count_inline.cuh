@@ -21,6 +21,8 @@
 #include "kernels.h"
 #include "table_inline.cuh"
 
+#include <cstdio>
+
 namespace gerbil {
 
 constexpr int kStageWords = 8;  // packed words staged per super-mer (≤ 256 bases)
@@ -120,6 +122,18 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
   // op 1 + s = claim slot s. A warp round never waits on a CAS: claims are
   // queued and 32 of them are issued together by one drain.
   auto push = [&](uint32_t mask, uint64_t k0, uint64_t k1, uint64_t b, uint32_t pq) {
+    // the queue is warp-shared state: every lane reaches each push / drain together (under
+    // independent thread scheduling a lane that left a divergent probe or emergency path late
+    // must not race the others' queue accesses; compute-sanitizer memcheck caught this with
+    // theta = 1 on over-full tables)
+    __syncwarp();
+#ifdef GERBIL_QDEBUG
+    {
+      int pred = 0;
+      __match_all_sync(0xffffffffu, qn, &pred);
+      if (qn + __popc(mask) > kQueue || !pred) printf("push: qn=%u mask=%08x lane=%u blk=%d\n", qn, mask, lane, blockIdx.x);
+    }
+#endif
     if ((mask >> lane) & 1u) {
       const uint32_t i = qn + __popc(mask & ((1u << lane) - 1u));
       q.k0[i] = k0;
@@ -159,6 +173,15 @@ __global__ void __launch_bounds__(128) count_inline_kernel(CountArgs a) {
   };
   // one memory round trip for `n` queued entries taken from the top (lanes < n)
   auto drain_n = [&](uint32_t n) {
+    __syncwarp();
+
+#ifdef GERBIL_QDEBUG
+    {
+      int pred = 0;
+      __match_all_sync(0xffffffffu, qn, &pred);
+      if (qn < n || qn > kQueue || !pred) printf("drain: qn=%u n=%u lane=%u blk=%d\n", qn, n, lane, blockIdx.x);
+    }
+#endif
     const uint32_t base = qn - n;
     const bool mine = lane < n;
     uint64_t k0 = 0, k1 = 0, b = 0;

@@ -118,6 +118,7 @@ struct GroupShuffleArgs {
   unsigned long long* off;      // [n_bins + 1] first descriptor of each bin (out)
   unsigned long long* win;      // [n_bins] windows per bin (out)
   unsigned long long* scratch;  // group_shuffle_scratch_bytes(n_bins)
+  uint64_t max_windows;         // bound on the windows of any one bin (picks 32-bit shared counters)
 };
 uint32_t group_shuffle_groups(uint32_t n_bins);
 size_t group_shuffle_scratch_bytes(uint32_t n_bins);
@@ -271,6 +272,14 @@ struct CompactArgs {
   unsigned long long* rec_n;
 };
 cudaError_t launch_compact(const CompactArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_store_u64(unsigned long long* dst_mapped, const unsigned long long* src, cudaStream_t s);
+cudaError_t launch_copy_words_mapped(unsigned long long* dst_mapped, const unsigned long long* src, uint64_t n,
+                                     cudaStream_t s);
+// App. C records of results [*lo, *hi) (device snapshots; at most max_n entries) appended to rec at a
+// byte range reserved on *rec_n (nothing is written past rec_cap; *rec_n counts every byte)
+cudaError_t launch_encode_records(const uint64_t* keys, const uint32_t* counts, const unsigned long long* lo,
+                                  const unsigned long long* hi, uint64_t max_n, uint32_t k, uint8_t* rec,
+                                  uint64_t rec_cap, unsigned long long* rec_n, int sms, cudaStream_t s);
 
 
 cudaError_t launch_clear_table(unsigned char* table, uint64_t bytes, int sms, cudaStream_t s);

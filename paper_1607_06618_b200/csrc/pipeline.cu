@@ -206,7 +206,7 @@ gerbil_status count_device_impl(gerbil_ctx* ctx, const uint64_t* codes, const ui
   // derives the bin histogram itself: step (b) then skips it. With world > 1 whole groups of
   // bins are exchanged (exchange_groups) and each owner plans its bins on the device.
   const uint64_t pos_lim = key_words(k) >= 4 ? (1ull << 39) : (1ull << 43);
-  const uint32_t smem_cap = (!ctx->rec_out && B >= kDevicePlanBins && B <= (1u << 22) && n_bases < pos_lim &&
+  const uint32_t smem_cap = (B >= kDevicePlanBins && B <= (1u << 22) && n_bases < pos_lim &&
                              (!ctx->comm || tot_bases < pos_lim))
                                 ? smem_slots_for(ctx, k)
                                 : 0u;

@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <type_traits>
+
 namespace gerbil {
 namespace {
 
@@ -174,7 +176,17 @@ __global__ void __launch_bounds__(256) group_hist_kernel(const uint32_t* __restr
   extern __shared__ uint32_t s_h[];
   for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) s_h[g] = 0;
   __syncthreads();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+  // 16-byte loads (4 bins) for the bulk, then the tail
+  const uint64_t n4 = n / 4, stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint4* b4 = reinterpret_cast<const uint4*>(bin);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const uint4 v = __ldg(b4 + i);
+    atomicAdd(&s_h[v.x >> kGroupShift], 1u);
+    atomicAdd(&s_h[v.y >> kGroupShift], 1u);
+    atomicAdd(&s_h[v.z >> kGroupShift], 1u);
+    atomicAdd(&s_h[v.w >> kGroupShift], 1u);
+  }
+  for (uint64_t i = 4 * n4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     atomicAdd(&s_h[__ldg(bin + i) >> kGroupShift], 1u);
   __syncthreads();
   for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
@@ -254,8 +266,11 @@ __global__ void __launch_bounds__(1024) part_setup_kernel(const unsigned long lo
 
 // One partition pass (A: n_seg == 1 over [0, n); B: n_seg segments from seg[], chunks
 // numbered per chunk_first[]). digit = (bin >> shift) & 63; cursors cur[seg * 64 + digit].
+#ifndef GERBIL_PART_MINB
+#define GERBIL_PART_MINB 2
+#endif
 template <bool PACK_OUT>
-__global__ void __launch_bounds__(kPartThreads) partition64_kernel(
+__global__ void __launch_bounds__(kPartThreads, GERBIL_PART_MINB) partition64_kernel(
     const uint64_t* __restrict__ desc_in, const uint32_t* __restrict__ bin_in, uint32_t n_seg,
     const unsigned long long* __restrict__ seg, const unsigned long long* __restrict__ chunk_first, uint32_t shift,
     unsigned long long* cur, uint64_t* __restrict__ desc_out, uint32_t* __restrict__ bin_out) {
@@ -339,14 +354,16 @@ __global__ void __launch_bounds__(kPartThreads) partition64_kernel(
 // then the scatter into bin order (descriptor bits 54.. cleared).
 constexpr int kFineT = 512;
 constexpr int kFineU = 8;
+template <bool WIDE>  // WIDE: a fine bin may hold >= 2^32 windows (u64 shared counters, CAS loops)
 __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t* __restrict__ desc_in,
                                                                  const unsigned long long* __restrict__ goff,
                                                                  uint32_t n_bins, unsigned long long* __restrict__ off,
                                                                  unsigned long long* __restrict__ win,
                                                                  uint64_t* __restrict__ desc_out) {
   constexpr uint32_t kFan = 1u << kGroupShift;
+  using WinT = typename std::conditional<WIDE, unsigned long long, uint32_t>::type;
   __shared__ uint32_t s_cur[kFan];
-  __shared__ unsigned long long s_win[kFan];
+  __shared__ WinT s_win[kFan];
   __shared__ uint32_t s_w[kFineT / 32];
   const uint32_t g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t b0 = g << kGroupShift;
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t*
       if (d[u] != ~0ull) {
         const uint32_t f = (uint32_t)(d[u] >> kDescPackShift);
         atomicAdd(&s_cur[f], 1u);
-        atomicAdd(&s_win[f], (unsigned long long)((d[u] & ((1u << kNwinBits) - 1)) + 1));
+        atomicAdd(&s_win[f], (WinT)((d[u] & ((1u << kNwinBits) - 1)) + 1));
       }
   }
   __syncthreads();
@@ -400,7 +417,7 @@ __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t*
     const uint32_t b = b0 + 2 * tid + q;
     if (b < n_bins) {
       off[b] = i0 + (q ? ex + x0 : ex);
-      win[b] = s_win[2 * tid + q];
+      win[b] = (unsigned long long)s_win[2 * tid + q];
     }
   }
   if (b0 + kFan >= n_bins && tid == 0) off[n_bins] = i1;  // the last group closes the offsets
@@ -573,8 +590,8 @@ cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_
     const size_t dyn = (size_t)G * 4;
     e = cudaFuncSetAttribute(group_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
-    uint64_t grid = (a.n + 255) / 256;
-    if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+    uint64_t grid = (a.n / 4 + 255) / 256 + 1;
+    if (grid > (uint64_t)sms * 8) grid = (uint64_t)sms * 8;
     group_hist_kernel<<<(unsigned)grid, 256, dyn, st>>>(a.bin_in, a.n, G, cnt);
   }
   part_setup_kernel<<<1, 1024, 0, st>>>(cnt, G, n_seg, goff, cur_a, cur_b, seg_b, chunk_b, a.n, seg_a, chunk_a);
@@ -600,7 +617,10 @@ cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_
   uint64_t* packed = n_seg > 1 ? a.desc_alt : a.tmp_desc;  // pass B output: never its own input
   partition64_kernel<true><<<(unsigned)grid, kPartThreads, kPartSmem, st>>>(pb_desc, pb_bin, n_seg, seg_b, chunk_b,
                                                                    kGroupShift, cur_b, packed, nullptr);
-  regroup_counted_kernel<<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);
+  if (a.max_windows >= (1ull << 32))
+    regroup_counted_kernel<true><<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);
+  else
+    regroup_counted_kernel<false><<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);
   return cudaGetLastError();
 }
 

@@ -109,7 +109,7 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #ifndef GERBIL_SM_MINB
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
-template <uint32_t ORD, int KMAX>
+template <uint32_t ORD, int KMAX, uint32_t MT>  // MT: m fixed at compile time (0 = runtime a.m)
 __global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,
                 int hist_smem) {
@@ -133,7 +133,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
   extern __shared__ uint32_t s_hist[];   // [2 or 3][n_bins] when hist_smem
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-  const uint32_t k = a.k, m = a.m, B = a.n_bins;
+  const uint32_t k = a.k, m = MT ? MT : a.m, B = a.n_bins;
   const uint32_t w = k - m + 1;
   const uint32_t n_keys = kSTile + k - m;  // m-mers needed by the tile's windows
   const uint64_t n_code_words = (a.n_bases + 31) / 32, n_mask_words = (a.n_bases + 63) / 64;
@@ -411,7 +411,14 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
     return cudaGetLastError();
   };
 #define GERBIL_SM_ORD(O) \
-  case O: return wide ? go(supermer_kernel<O, kMaxKAll>) : go(supermer_kernel<O, kMaxKSmall>)
+  case O: return wide ? go(supermer_kernel<O, kMaxKAll, 0>) : go(supermer_kernel<O, kMaxKSmall, 0>)
+  // the default ordering with the common minimizer lengths: shifts and masks as constants
+  if (a.ordering == kOrdKMC2 && !wide) {
+    if (a.m == 15) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 15>);
+    if (a.m == 11) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 11>);
+    if (a.m == 7) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 7>);
+  }
+  if (a.ordering == kOrdKMC2 && wide && a.m == 15) return go(supermer_kernel<kOrdKMC2, kMaxKAll, 15>);
   switch (a.ordering) {
     GERBIL_SM_ORD(kOrdKMC2);
     GERBIL_SM_ORD(kOrdLEX);

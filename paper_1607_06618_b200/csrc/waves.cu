@@ -63,17 +63,16 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
     CK(ctx->ovf.ensure(ovf_cap * W * 8));
     // Result buffer: the waves' distinct bound can exceed device memory when most k-mers are
     // singletons and min_count > 1 drops them (C4: ~1.5e10 bound, ~3.6e8 kept per GPU), so it is
-    // sized for at most a quarter of the free memory and grown between waves when the bound of
+    // sized for at most an eighth of the device memory and grown between waves when the bound of
     // the next wave might not fit (a sync reads how many results the earlier waves kept).
     uint64_t out_chunk = out_bound;
     {
-      size_t fr = 0, tot = 0;
-      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-        const uint64_t fit = (uint64_t)(fr / 4) / (W * 8 + 4);
-        uint64_t big_wave = 0;
-        for (const Wave& wv : waves) big_wave = std::max(big_wave, std::min<uint64_t>(wv.nb * kSlotsPerBucket, wv.windows));
-        out_chunk = std::min(out_bound, std::max(fit, 2 * big_wave));
-      }
+      // a fixed share of the device memory (not of what is free right now: a budget that moved
+      // between calls would re-allocate — and copy — the result buffer every call)
+      const uint64_t fit = result_budget_entries(ctx, W, 8);
+      uint64_t big_wave = 0;
+      for (const Wave& wv : waves) big_wave = std::max(big_wave, std::min<uint64_t>(wv.nb * kSlotsPerBucket, wv.windows));
+      out_chunk = std::min(out_bound, std::max(fit, 2 * big_wave));
     }
     uint64_t out_cap = pre.out_n + out_chunk + ovf_cap;
     CK(ensure_keep(ctx->out_keys, out_cap * W * 8, pre.out_n * W * 8, ctx->stream));
@@ -388,14 +387,9 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   const uint32_t W = key_words(k);
   CK(ctx->smem_failed.ensure((size_t)n * 16 + 16));
   // the shared-memory pass writes at most out_bound results, but with min_count > 1 on singleton-rich
-  // input (C4) that bound can exceed device memory: the buffer is capped at a quarter of the free
+  // input (C4) that bound can exceed device memory: the buffer is capped at a fifth of the device
   // memory and, if the kept results do not fit, the pass is rerun once with the exact size
-  uint64_t out_cap = std::max<uint64_t>(out_bound, 1);
-  {
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
-      out_cap = std::min<uint64_t>(out_cap, std::max<uint64_t>(1, (uint64_t)(fr / 4) / (W * 8 + 4)));
-  }
+  uint64_t out_cap = std::min<uint64_t>(std::max<uint64_t>(out_bound, 1), result_budget_entries(ctx, W, 5));
   CK(ctx->out_keys.ensure(out_cap * W * 8));
   CK(ctx->out_counts.ensure(out_cap * 4));
   CK(ctx->counters.ensure(sizeof(Counters)));
@@ -417,16 +411,81 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   a.failed = ctx->smem_failed.as<unsigned long long>();
   a.n_failed = &dc->read_work;
   Counters& hc = *ctx->h_counters;
+  // Streaming call (gerbil_count_host_stream): the shared-memory pass runs in slices of the bin
+  // list; after each slice its results are encoded as App. C records (encode_records on the lane
+  // stream, while the next slice counts) and copied to the caller's page-locked buffer on the copy
+  // stream — the D2H of slice s overlaps the counting of slices s+1.. .
+  const bool streaming = ctx->rec_out != nullptr;
+  const uint64_t rec_max = 5 + (k + 3) / 4;
+  uint64_t host_off = ctx->rec_base, rec_done = 0;
+  int n_slices = 0;
+  auto stream_slices = [&](const SmemCountArgs& as, uint32_t list_n, int S) -> gerbil_status {
+    CK(ctx->rec_snap_d.ensure((size_t)(S + 1) * 8));
+    unsigned long long* snap = ctx->rec_snap_d.as<unsigned long long>();
+    CK(cudaMemcpyAsync(snap, &dc->out_n, 8, cudaMemcpyDeviceToDevice, ctx->stream));  // slice 0 start
+    if (ctx->h_snap_n < (size_t)S) {
+      if (ctx->h_snap) cudaFreeHost(ctx->h_snap);
+      ctx->h_snap = nullptr;
+      ctx->h_snap_n = 0;
+      CK(cudaMallocHost((void**)&ctx->h_snap, (size_t)S * 8));
+      ctx->h_snap_n = S;
+    }
+    while (ctx->wave_ev.size() < (size_t)2 * S) {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx->wave_ev.push_back(ev);
+    }
+    unsigned long long* rec_ctr = ctx->rec_meta.as<unsigned long long>();
+    for (int q = 0; q < S; ++q) {
+      const uint32_t i0 = (uint32_t)((uint64_t)list_n * q / S), i1 = (uint32_t)((uint64_t)list_n * (q + 1) / S);
+      SmemCountArgs sl = as;
+      sl.range = as.range + 2 * (size_t)i0;
+      sl.n_list = i1 - i0;
+      {
+        Timer tm(ctx, K_SMEM);
+        CK(launch_count_smem(sl, ctx->sms, ctx->stream));
+      }
+      CK(cudaMemcpyAsync(snap + q + 1, &dc->out_n, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaEventRecord(ctx->wave_ev[2 * q], ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->lane_stream, ctx->wave_ev[2 * q], 0));
+      CK(launch_encode_records(as.out_keys, as.out_counts, snap + q, snap + q + 1, as.out_cap, k,
+                               ctx->rec_stage2.as<uint8_t>(), ctx->rec_stage2.bytes, rec_ctr, ctx->sms,
+                               ctx->lane_stream));
+      unsigned long long* hs = nullptr;
+      CK(cudaHostGetDevicePointer((void**)&hs, ctx->h_snap + q, 0));
+      CK(launch_store_u64(hs, rec_ctr, ctx->lane_stream));
+      CK(cudaEventRecord(ctx->wave_ev[2 * q + 1], ctx->lane_stream));
+    }
+    for (int q = 0; q < S; ++q) {  // copy each slice's records once they exist
+      CK(cudaEventSynchronize(ctx->wave_ev[2 * q + 1]));
+      const uint64_t end = ctx->h_snap[q], len = end - rec_done;
+      if (len && host_off + len <= ctx->rec_cap)
+        CK(cudaMemcpyAsync(ctx->rec_out + host_off, ctx->rec_stage2.as<uint8_t>() + rec_done, len,
+                           cudaMemcpyDeviceToHost, ctx->pcie_stream));
+      rec_done = end;
+      host_off += len;
+    }
+    n_slices += S;
+    return GERBIL_OK;
+  };
+  if (streaming) {
+    CK(ctx->rec_stage2.ensure(std::max<uint64_t>(out_cap, 1) * rec_max + 64));
+    CK(ctx->rec_meta.ensure(2 * 8));
+    CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->pcie_stream));  // the staging buffer's previous readers are done
+  }
   for (int attempt = 0;; ++attempt) {
     a.out_keys = ctx->out_keys.as<uint64_t>();
     a.out_counts = ctx->out_counts.as<uint32_t>();
     a.out_cap = out_cap;
-    {
+    if (streaming) {
+      CKS(stream_slices(a, n, 16));
+    } else {
       Timer tm(ctx, K_SMEM);
       CK(launch_count_smem(a, ctx->sms, ctx->stream));
     }
     trace("smem count issued");
-    CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
     CK(cudaStreamSynchronize(ctx->stream));
     trace("smem count done (synced)");
     if (hc.out_n > out_bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
@@ -435,6 +494,13 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
     out_cap = hc.out_n;  // exact: the rerun keeps the same k-mers
     CK(ctx->out_keys.ensure(out_cap * W * 8));
     CK(ctx->out_counts.ensure(out_cap * 4));
+    if (streaming) {  // the records of the first attempt are incomplete: stream them again
+      CK(cudaStreamSynchronize(ctx->pcie_stream));
+      host_off = ctx->rec_base;
+      rec_done = 0;
+      CK(ctx->rec_stage2.ensure(out_cap * rec_max + 64));
+      CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+    }
     CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
   }
   const uint64_t n_failed = hc.read_work;
@@ -444,9 +510,10 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   pre.distinct = hc.distinct;
   uint64_t failed_windows = 0;
   if (n_failed) {
-    std::vector<unsigned long long> fr(2 * n_failed);
-    CK(cudaMemcpyAsync(fr.data(), ctx->smem_failed.p, fr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx->h_fail.ensure(2 * n_failed * 8));
+    CK(d2h_small(ctx, ctx->h_fail.p, ctx->smem_failed.p, 2 * n_failed * 8));
     CK(cudaStreamSynchronize(ctx->stream));
+    const unsigned long long* fr = ctx->h_fail.as<unsigned long long>();
     for (uint64_t i = 0; i < n_failed; ++i) {
       const uint64_t w = fr[2 * i + 1] >> kRangeWinShift;
       rest.push_back({fr[2 * i], fr[2 * i + 1] & kRangeEndMask, w});
@@ -497,11 +564,13 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       a2.out_counts = ctx->out_counts.as<uint32_t>();
       a2.out_cap = out2;
       a2.failed = ctx->smem_failed.as<unsigned long long>();
-      {
+      if (streaming) {
+        CKS(stream_slices(a2, (uint32_t)n2, 1));
+      } else {
         Timer tm(ctx, K_SMEM);
         CK(launch_count_smem(a2, ctx->sms, ctx->stream));
       }
-      CK(cudaMemcpyAsync(ctx->h_counters, dc, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
       CK(cudaStreamSynchronize(ctx->stream));
       if (hc.out_n > out2) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
       pre.out_n = hc.out_n;
@@ -510,9 +579,10 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       const uint64_t nf2 = hc.read_work;
       uint64_t fw2 = 0;
       if (nf2) {
-        std::vector<unsigned long long> fr(2 * nf2);
-        CK(cudaMemcpyAsync(fr.data(), ctx->smem_failed.p, fr.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx->h_fail.ensure(2 * nf2 * 8));
+        CK(d2h_small(ctx, ctx->h_fail.p, ctx->smem_failed.p, 2 * nf2 * 8));
         CK(cudaStreamSynchronize(ctx->stream));
+        const unsigned long long* fr = ctx->h_fail.as<unsigned long long>();
         for (uint64_t i = 0; i < nf2; ++i) {
           const uint64_t w = fr[2 * i + 1] >> kRangeWinShift;
           keep.push_back({fr[2 * i], fr[2 * i + 1] & kRangeEndMask, w});
@@ -529,6 +599,13 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   ctx->stats.smem_windows += smem_windows;
   const double smem_obs = smem_windows ? (double)pre.distinct / (double)smem_windows : 0.0;
   gerbil_status st = GERBIL_OK;
+  if (streaming) {
+    ctx->rec_base = host_off;  // the L2 waves append their records after the shared-memory pass's
+    if (rest.empty()) {
+      CK(cudaStreamSynchronize(ctx->pcie_stream));
+      ctx->rec_bytes = host_off;
+    }
+  }
   if (rest.empty()) {
     ctx->stats.waves = 0;
     ctx->stats.ratio_used = ctx->rho;
@@ -583,7 +660,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
                           const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,
                           const std::vector<uint32_t>& bins, uint32_t k, uint32_t min_count,
                           uint64_t total_windows) {
-  const uint32_t cap = ctx->rec_out ? 0u : smem_slots_for(ctx, k);
+  const uint32_t cap = smem_slots_for(ctx, k);
   ctx->stats.smem_slots = cap;
   if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
                                       total_windows, Preset{});
@@ -629,7 +706,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
 // (c) on one rank: group-major shuffle (shuffle.cu) of desc_in/bin_in into ctx->desc_sorted; the
 // bins' offsets (ctx->bin_off_d) and windows (ctx->hist) come out of it. tmp_* are scratch of n.
 gerbil_status group_shuffle(gerbil_ctx* ctx, const uint64_t* desc_in, const uint32_t* bin_in, uint64_t n, uint32_t B,
-                            uint64_t* tmp_desc, uint32_t* tmp_bin, uint64_t* desc_alt) {
+                            uint64_t* tmp_desc, uint32_t* tmp_bin, uint64_t* desc_alt, uint64_t max_windows) {
   if (n >= (1ull << 32)) return fail(ctx, GERBIL_E_USAGE, "more than 2^32 super-mers in one call: split the batch");
   CK(ctx->hist.ensure(3ull * B * 8));
   CK(ctx->bin_off_d.ensure(((size_t)B + 1) * 8));
@@ -647,6 +724,7 @@ gerbil_status group_shuffle(gerbil_ctx* ctx, const uint64_t* desc_in, const uint
   gs.off = ctx->bin_off_d.as<unsigned long long>();
   gs.win = ctx->hist.as<unsigned long long>();
   gs.scratch = ctx->p_tmp.as<unsigned long long>();
+  gs.max_windows = max_windows;
   const uint32_t G = group_shuffle_groups(B);
   Timer tm(ctx, K_SHUFFLE, nullptr, true, G > 64 ? 5 : 4);
   CK(launch_group_shuffle(gs, ctx->sms, ctx->stream));
@@ -663,7 +741,7 @@ gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, ui
   CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));  // scratch (reuses the exchange buffers)
   CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
   CKS(group_shuffle(ctx, ctx->desc_pre.as<uint64_t>(), ctx->bin_pre.as<uint32_t>(), n_sm, B,
-                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>()));
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>(), windows));
   return count_planned(ctx, codes, B, cap, k, min_count, windows);
 }
 
@@ -683,7 +761,8 @@ gerbil_status exchange_groups(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n
   CK(ctx->send_desc.ensure(std::max<uint64_t>(n_sm, 1) * 8));
   CK(ctx->send_bin.ensure(std::max<uint64_t>(n_sm, 1) * 4));
   CKS(group_shuffle(ctx, ctx->desc_pre.as<uint64_t>(), ctx->bin_pre.as<uint32_t>(), n_sm, B,
-                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>()));
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->desc_pre.as<uint64_t>(),
+                    ctx->stats.valid_windows));
   // per-group statistics of every rank
   CK(ctx->hist_all.ensure(3ull * G * 8 * (P + 1)));
   unsigned long long* gst = ctx->hist_all.as<unsigned long long>();
@@ -774,7 +853,8 @@ gerbil_status exchange_groups(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n
   ctx->stats.bytes_recv = (n_recv - (rd_off[r + 1] - rd_off[r])) * 12 + (w_recv - (rw_off[r + 1] - rw_off[r])) * 8;
   // regroup what this rank owns by bin, then count it
   CKS(group_shuffle(ctx, ctx->recv_desc.as<uint64_t>(), ctx->recv_bin.as<uint32_t>(), n_recv, B,
-                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->recv_desc.as<uint64_t>()));
+                    ctx->send_desc.as<uint64_t>(), ctx->send_bin.as<uint32_t>(), ctx->recv_desc.as<uint64_t>(),
+                    owned_windows));
   return count_planned(ctx, ctx->recv_payload.as<uint64_t>(), B, cap, k, min_count, owned_windows);
 }
 

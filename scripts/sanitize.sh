@@ -8,7 +8,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report analysis"
   timeout 1500 compute-sanitizer --tool $tool $extra --error-exitcode 9 --kernel-name-exclude kns=synth \
-     python scripts/sanitize_cases.py ${CASES:-} > gpurun_out/sanitize_$tool.log 2>&1
+     python scripts/sanitize_cases.py ${CASES:-smem_k40 smem_k65_mc2 smem_alla ref_k150 ref_alla l2_k28 l2_k40 l2_k200} > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$?" >> gpurun_out/summary.txt
   tail -3 gpurun_out/sanitize_$tool.log >> gpurun_out/summary.txt
 done

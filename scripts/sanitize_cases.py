@@ -27,6 +27,12 @@ CASES = {
     "l2_k200": (lambda: synth.fastx(LONG, synth.FASTA), 200, 11, 2, dict(n_bins=16, count_mode=gerbil.COUNT_L2)),
     "l2_overflow": (lambda: synth.fastx(C0, synth.FASTQ), 33, 9, 1,
                     dict(n_bins=4, count_mode=gerbil.COUNT_L2, max_probes=1, target_load=1.6, distinct_ratio=0.3)),
+    "l2_overflow_k28": (lambda: synth.fastx(C0, synth.FASTQ), 28, 9, 1,
+                        dict(n_bins=4, count_mode=gerbil.COUNT_L2, max_probes=1, target_load=1.6, distinct_ratio=0.3)),
+    "l2_overflow_k40_p4": (lambda: synth.fastx(C0, synth.FASTQ), 40, 9, 1,
+                           dict(n_bins=4, count_mode=gerbil.COUNT_L2, max_probes=4, target_load=1.2,
+                                distinct_ratio=0.3)),
+    "l2_k40": (lambda: synth.fastx(C0, synth.FASTQ), 40, 9, 1, dict(n_bins=4, count_mode=gerbil.COUNT_L2)),
 }
 
 
