@@ -48,6 +48,7 @@ gerbil_status gerbil_init(const gerbil_config* cfg_in, gerbil_ctx** out) {
   gerbil_ctx* ctx = new gerbil_ctx();
   ctx->cfg = cfg;
   ctx->rho = cfg.distinct_ratio > 0 ? cfg.distinct_ratio : 0.5;
+  ctx->rho_seen = cfg.distinct_ratio > 0;
   ctx->rank = cfg.rank;
   ctx->world = cfg.world;
   cudaError_t e = cudaSuccess;

@@ -205,6 +205,7 @@ struct gerbil_ctx {
   bool poisoned = false;
   std::string err;
   double rho = 0.5;
+  bool rho_seen = false;  // rho was measured (an earlier call) or given (cfg.distinct_ratio)
   Comm* comm = nullptr;
   int rank = 0, world = 1;
   // device buffers
@@ -324,6 +325,13 @@ inline gerbil_status validate(gerbil_ctx* ctx, uint32_t k, uint32_t& m, uint32_t
 }
 
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k);
+// The first counting tier uses the CTA-wide reference tables (count_ref.cu) for long keys
+// (W >= 4), per-warp tables of whole keys otherwise (measured: for W <= 3 the reference tables
+// as first tier cost 1.5-2x on the C2/C3 shards; they serve as the second tier there).
+inline bool ref_tier1(const gerbil_ctx* ctx, uint32_t k) {
+  (void)ctx;
+  return key_words(k) >= 4;
+}
 // from this many bins up, a single rank plans steps (c)-(e) on the device
 constexpr uint32_t kDevicePlanBins = 1u << 16;
 gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,
@@ -469,7 +477,7 @@ inline cudaError_t ensure_keep(DevBuf& b, size_t n, size_t keep, cudaStream_t s)
 struct Preset;
 struct RestBin;
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k);
-uint32_t smem_max_fill(uint32_t cap, uint32_t k);
+uint32_t smem_max_fill(const gerbil_ctx* ctx, uint32_t cap, uint32_t k);
 uint64_t smem_window_threshold(const gerbil_ctx* ctx, uint32_t max_fill);
 gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const uint64_t* desc,
                           const std::vector<uint64_t>& bin_off, const std::vector<uint64_t>& bin_win,

@@ -315,6 +315,9 @@ uint32_t ref_max_fill(uint32_t cap) {
 cudaError_t launch_count_ref(const SmemCountArgs& a, int sms, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
   switch (key_words(a.k)) {
+    case 1: return launch_ref_w<1>(a, sms, st);
+    case 2: return launch_ref_w<2>(a, sms, st);
+    case 3: return launch_ref_w<3>(a, sms, st);
     case 4: return launch_ref_w<4>(a, sms, st);
     case 5: return launch_ref_w<5>(a, sms, st);
     case 6: return launch_ref_w<6>(a, sms, st);

@@ -581,7 +581,7 @@ cudaError_t launch_plan_bins(const PlanBinsArgs& a, int sms, cudaStream_t st) {
 
 cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t st) {
   if (a.n_list == 0) return cudaSuccess;
-  if (key_words(a.k) >= 4) return launch_count_ref(a, sms, st);  // CTA-wide reference tables
+  if (key_words(a.k) >= 4 || a.warps < 0) return launch_count_ref(a, sms, st);  // CTA-wide reference tables
   switch (key_words(a.k)) {
     case 1: return launch_smem<1, true>(a, sms, st);
     case 2: return smem_pack(a.k) ? launch_smem<2, true>(a, sms, st) : launch_smem<2, false>(a, sms, st);

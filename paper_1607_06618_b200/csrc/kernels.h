@@ -203,7 +203,8 @@ struct SmemCountArgs {
   unsigned long long* failed;        // [n_list][2] range entries of abandoned bins
   unsigned long long* n_failed;
   uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 8 = full-size tables
-  int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match
+  int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match; -1 = the
+                                     // CTA-wide reference tables of count_ref.cu (any W)
 };
 // Table slots a bin of `win` windows gets (count_smem_kernel): windows * 1.25 + 32, rounded up to 32,
 // capped at the warp's table (cap).

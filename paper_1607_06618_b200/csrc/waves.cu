@@ -329,7 +329,10 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
     }
     if (hc.out_n > out_cap) return fail(ctx, GERBIL_E_INTERNAL, "result buffer bound violated");
     // ratio adaptation for the next call ("we dynamically adjust the ratio")
-    if (observed > 0) ctx->rho = std::min(1.0, std::max(observed * 1.15 + 0.01, 0.02));
+    if (observed > 0) {
+      ctx->rho = std::min(1.0, std::max(observed * 1.15 + 0.01, 0.02));
+      ctx->rho_seen = true;
+    }
     ctx->n_out = hc.out_n;
     if (streaming) {  // wait for the last record copies
       CK(cudaStreamSynchronize(ctx->pcie_stream));
@@ -352,16 +355,17 @@ uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
     cudaGetLastError();
     return 0;
   }
-  // W >= 4: one CTA-wide table of occurrence references per bin (count_ref.cu)
-  const uint32_t cap = key_words(k) >= 4 ? ref_table_slots((size_t)ctx->smem_optin - 1024)
+  // W >= 4, or mostly distinct k-mers: one CTA-wide table of occurrence references per bin
+  // (count_ref.cu); else per-warp tables of whole keys (count_smem.cu)
+  const uint32_t cap = ref_tier1(ctx, k) ? ref_table_slots((size_t)ctx->smem_optin - 1024)
                                          : smem_table_slots(k, (size_t)ctx->smem_optin - 1024);
   return cap >= 128 ? cap : 0;
 }
 
-// Abandonment threshold of the shared-memory tables: a round inserts <= 32 k-mers, so
+// Abandonment threshold of the shared-memory tables: a round inserts <= 32 k-mers per warp, so
 // a table never fills.
-uint32_t smem_max_fill(uint32_t cap, uint32_t k) {
-  return key_words(k) >= 4 ? ref_max_fill(cap) : cap - std::max<uint32_t>(64u, cap / 4);
+uint32_t smem_max_fill(const gerbil_ctx* ctx, uint32_t cap, uint32_t k) {
+  return ref_tier1(ctx, k) ? ref_max_fill(cap) : cap - std::max<uint32_t>(64u, cap / 4);
 }
 
 // Windows up to which a bin goes to the shared-memory pass: predicted distinct
@@ -405,6 +409,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   a.canonical = ctx->cfg.disable_normalization ? 0u : 1u;
   a.cap = cap;
   a.max_fill = max_fill;
+  a.warps = ref_tier1(ctx, k) ? -1 : 0;  // -1: CTA-wide reference tables
   a.out_n = &dc->out_n;
   a.sum_counts = &dc->sum_counts;
   a.distinct = &dc->distinct;
@@ -459,6 +464,10 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
     for (int q = 0; q < S; ++q) {  // copy each slice's records once they exist
       CK(cudaEventSynchronize(ctx->wave_ev[2 * q + 1]));
       const uint64_t end = ctx->h_snap[q], len = end - rec_done;
+      if (end < rec_done || end > ctx->rec_stage2.bytes)
+        return fail(ctx, GERBIL_E_INTERNAL, "record stream: slice " + std::to_string(q) + "/" + std::to_string(S) +
+                                                " end " + std::to_string(end) + " < done " + std::to_string(rec_done) +
+                                                " or > staging " + std::to_string(ctx->rec_stage2.bytes));
       if (len && host_off + len <= ctx->rec_cap)
         CK(cudaMemcpyAsync(ctx->rec_out + host_off, ctx->rec_stage2.as<uint8_t>() + rec_done, len,
                            cudaMemcpyDeviceToHost, ctx->pcie_stream));
@@ -523,13 +532,20 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   ctx->stats.smem_bins += n;
   ctx->stats.smem_failed += n_failed;
   uint64_t smem_windows = elig_windows - std::min(elig_windows, failed_windows);
-  // Tier 2: bins too large for the many-warp tables get 4-warp tables (~4x the slots per
-  // warp) in a second launch; what still does not fit goes to the wave tables.
-  const int w1 = a.warps ? a.warps : smem_count_warps(k);
+  // Tier 2 (W <= 3): bins too large for the per-warp tables get a second launch — with mostly
+  // repeated k-mers (rho < 0.35, e.g. C1) on half as many warps (twice the slots per warp),
+  // with mostly distinct ones (C2/C3 shards) on one CTA-wide table of occurrence references per
+  // bin (count_ref.cu, ~16K slots: verification re-reads cost little when repeats are rare);
+  // what still does not fit goes to the wave tables. (W >= 4: tier 1 already is that table.)
+  const bool tier1_ref = ref_tier1(ctx, k);
+  const bool tier2_ref = !tier1_ref && W <= 3 && ctx->rho > 0.35;
+  const int w1 = a.warps > 0 ? a.warps : smem_count_warps(k);
   const int w2n = std::max(1, w1 / 2);
-  const uint32_t cap2 = w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u;
+  const uint32_t cap2 = tier1_ref ? 0u
+                        : tier2_ref ? ref_table_slots((size_t)ctx->smem_optin - 1024)
+                                    : (w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u);
   if (!rest.empty() && cap2 > cap) {
-    const uint32_t mf2 = smem_max_fill(cap2, k);
+    const uint32_t mf2 = tier2_ref ? ref_max_fill(cap2) : cap2 - std::max<uint32_t>(64u, cap2 / 4);
     const uint64_t thr2 = smem_window_threshold(ctx, mf2);
     std::vector<RestBin> keep;
     uint64_t n2 = 0, w2 = 0, ob2 = 0;
@@ -559,12 +575,16 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       a2.n_list = (uint32_t)n2;
       a2.cap = cap2;
       a2.max_fill = mf2;
-      a2.warps = w2n;
+      a2.warps = tier2_ref ? -1 : w2n;  // -1: the CTA-wide reference tables
       a2.out_keys = ctx->out_keys.as<uint64_t>();
       a2.out_counts = ctx->out_counts.as<uint32_t>();
       a2.out_cap = out2;
       a2.failed = ctx->smem_failed.as<unsigned long long>();
-      if (streaming) {
+      if (streaming) {  // tier 1's records are copied out: tier 2's start a fresh staging area
+        CK(cudaStreamSynchronize(ctx->pcie_stream));
+        rec_done = 0;
+        CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+        CK(ctx->rec_stage2.ensure(std::max<uint64_t>(ob2, 1) * rec_max + 64));
         CKS(stream_slices(a2, (uint32_t)n2, 1));
       } else {
         Timer tm(ctx, K_SMEM);
@@ -648,7 +668,10 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
     if (st != GERBIL_OK) return st;
   }
   // ratio adaptation: the larger of the wave and shared-memory observations
-  if (smem_obs > 0) ctx->rho = std::min(1.0, std::max(rest.empty() ? 0.0 : ctx->rho, std::max(smem_obs * 1.15 + 0.01, 0.02)));
+  if (smem_obs > 0) {
+    ctx->rho = std::min(1.0, std::max(rest.empty() ? 0.0 : ctx->rho, std::max(smem_obs * 1.15 + 0.01, 0.02)));
+    ctx->rho_seen = true;
+  }
   return st;
 }
 
@@ -664,7 +687,7 @@ gerbil_status count_waves(gerbil_ctx* ctx, const uint64_t* stream_codes, const u
   ctx->stats.smem_slots = cap;
   if (cap == 0) return count_waves_l2(ctx, stream_codes, desc, bin_off, bin_win, bins, k, min_count,
                                       total_windows, Preset{});
-  const uint32_t max_fill = smem_max_fill(cap, k);
+  const uint32_t max_fill = smem_max_fill(ctx, cap, k);
   const uint64_t thr = smem_window_threshold(ctx, max_fill);
   std::vector<uint32_t> elig;
   std::vector<RestBin> rest;
@@ -866,7 +889,7 @@ gerbil_status count_planned(gerbil_ctx* ctx, const uint64_t* codes, uint32_t B, 
   unsigned long long* d_win = ctx->hist.as<unsigned long long>();
   unsigned long long* d_off = ctx->bin_off_d.as<unsigned long long>();
   trace("scatter issued");
-  const uint32_t max_fill = smem_max_fill(cap, k);
+  const uint32_t max_fill = smem_max_fill(ctx, cap, k);
   CK(ctx->smem_range.ensure((size_t)B * 16));
   CK(ctx->rest_range.ensure((size_t)B * 24));
   CK(ctx->plan_sums.ensure(5 * 8));
