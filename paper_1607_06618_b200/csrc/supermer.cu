@@ -195,16 +195,15 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
       // initial m-mer at j0
       const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
       const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
-      uint32_t f = (uint32_t)(v >> (64 - 2 * m));
-      uint32_t rc = (uint32_t)(rev_pairs(~v & (~0ull << (64 - 2 * m))) & mmask);
+      // the block's bases j0 .. j0+kKB-1+m-1 (<= 26) all sit in v; R = reverse complement of v's
+      // 32 bases, so the m-mer at i is bits [64-2(i+m), 64-2i) of v and its reverse complement
+      // bits [2i, 2i+2m) of R — independent extractions (no rolling dependency chain)
+      const uint64_t R = rev_pairs(~v);
       uint32_t c[kKB];
 #pragma unroll
       for (int i = 0; i < kKB; ++i) {
-        if (i > 0) {  // the block's bases j0 .. j0+kKB-1+m-1 (<= 24) all sit in v
-          const uint32_t nb = (uint32_t)(v >> (62 - 2 * (i + m - 1))) & 3u;
-          f = ((f << 2) | nb) & mmask;
-          rc = (rc >> 2) | ((3u - nb) << (2 * m - 2));
-        }
+        const uint32_t f = (uint32_t)(v >> (64 - 2 * (i + m))) & mmask;
+        const uint32_t rc = (uint32_t)(R >> (2 * i)) & mmask;
         const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
         c[i] = kf < kr ? kf : kr;
       }
