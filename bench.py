@@ -231,12 +231,15 @@ def stream_model(st: dict, k: int, P: int, alpha: float = 0.7) -> dict:
 
 
 def _traffic_table() -> dict:
+    """ncu-measured DRAM traffic / instruction counts per kernel for this configuration
+    (profiles/roofline_traffic.json, written by scripts/roofline_traffic.py from the committed
+    ncu captures), keyed by (config, k, m) so that a relabelled workload still matches."""
     out = {}
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         for e in (tj if isinstance(tj, list) else [tj]):
-            if e.get("workload") == WORKLOAD_NAME:
+            if e.get("config") == CFG.name and e.get("k") == K and e.get("m") == M:
                 out[e.get("kernel")] = e
     return out
 
@@ -248,7 +251,9 @@ def roofline_report(st: dict, ms: float, per_kernel: dict, steps: int, P: int) -
     n_k = max(float(st["valid_windows"]), 1.0)
     smem_share = st["smem_windows"] / n_k
     if smem_share >= 0.5:
-        kname, key, launches, kms = "count_smem_kernel", "smem", st["launches_smem"], per_kernel["smem"][0] / steps
+        # W >= 4: the CTA-wide reference tables (count_ref.cu) are the shared-memory tier
+        kname = "count_ref_kernel" if int(st["W"]) >= 4 else "count_smem_kernel"
+        key, launches, kms = "smem", st["launches_smem"], per_kernel["smem"][0] / steps
         units = float(st["smem_windows"])
     else:
         kname, key, launches, kms = "count_inline_kernel", "count", st["launches_count"], per_kernel["count"][0] / steps
@@ -281,7 +286,7 @@ def roofline_report(st: dict, ms: float, per_kernel: dict, steps: int, P: int) -
         "model": "SURVEY.md §8(d) stream model: 0.25b + 2(1+(P-1)/P)(0.25Eb + 8n_s) + 2Sd/alpha + (8W+4)d_kept; "
                  "random-sector model adds 64 n_k"}
     # what actually binds the shared-memory kernel: instruction issue (ncu)
-    if kname == "count_smem_kernel" and tr.get("warp_inst_per_step"):
+    if kname in ("count_smem_kernel", "count_ref_kernel") and tr.get("warp_inst_per_step"):
         sms, clk = 148, tr.get("sm_mhz", 1965.0) * 1e6
         wi = float(tr["warp_inst_per_step"])
         roof["issue"] = {
