@@ -76,7 +76,9 @@ def _run(world: int, n_bins: int, tmp_path):
     return z["H"], list(z["plans"])
 
 
-@pytest.mark.parametrize("world,n_bins", [(2, 512), (2, 1), (3, 97)])
+# (2, 4096): the group-level plan of the device-planned multi-GPU path — 2^22 bins exchanged as
+# 4096 groups of 1024 bins (waves.cu exchange_groups runs exchange_plan over group histograms)
+@pytest.mark.parametrize("world,n_bins", [(2, 512), (2, 1), (3, 97), (2, 4096), (3, 4096)])
 def test_exchange_plan_consistent_across_gloo_ranks(world, n_bins, tmp_path):
     H, plans = _run(world, n_bins, tmp_path)
     P, B = world, n_bins
@@ -99,6 +101,11 @@ def test_exchange_plan_consistent_across_gloo_ranks(world, n_bins, tmp_path):
             assert sd[s][d + 1] - sd[s][d] == expect
     total_sm = int(H[:, 1].sum())
     assert sum(int(rd[d][P]) for d in range(P)) == total_sm == sum(int(sd[s][P]) for s in range(P))
+    # each rank's data lands, in d's receive buffer, after the lower ranks' (the receive base the
+    # group exchange computes on the sending side)
+    for d in range(P):
+        for s in range(P):
+            assert rw[d][s] == sum(int(sw[q][d + 1] - sw[q][d]) for q in range(s))
     # LPT balance on windows
     gw = H[:, 0].sum(axis=0).astype(np.float64)
     load = np.array([gw[owner == d].sum() for d in range(P)])
