@@ -41,14 +41,10 @@ constexpr uint32_t kFull = 0xffffffffu;
 #ifndef GERBIL_REF_CTAS
 #define GERBIL_REF_CTAS 1
 #endif
-#ifndef GERBIL_REF_SEG
-#define GERBIL_REF_SEG 1
-#endif
 constexpr int kRefThreads = GERBIL_REF_THREADS;  // warps per bin = kRefThreads / 32
 constexpr int kRefWarps = kRefThreads / 32;
 constexpr int kRefCtasPerSm = GERBIL_REF_CTAS;   // bins in flight per SM
-constexpr uint32_t kSeg = GERBIL_REF_SEG;        // windows per lane segment (one extraction, then rolling)
-constexpr uint32_t kSegUnit = 24;                // segments per warp work unit (target)
+constexpr uint32_t kLongSm = 32;                 // mean windows per super-mer from which a bin is cut in pieces
 constexpr uint64_t kOcc = 1ull << 63;
 constexpr int kFpShift = 40;
 constexpr uint64_t kPosMask = (1ull << 39) - 1;
@@ -86,6 +82,9 @@ __global__ void __launch_bounds__(kRefThreads, kRefCtasPerSm) count_ref_kernel(S
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_ref + cap);
   uint16_t* s_list = reinterpret_cast<uint16_t*>(s_cnt + cap);
   __shared__ uint32_t s_nd, s_unit, s_keep, s_ocur;
+  __shared__ uint64_t s_dsc[kRefThreads];   // long super-mers: a batch of descriptors
+  __shared__ uint32_t s_pfx[kRefThreads];   // and the first piece of each
+  __shared__ uint32_t s_wsum[kRefWarps];
   __shared__ int s_abandon;
   __shared__ unsigned long long s_obase;
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
@@ -98,11 +97,7 @@ __global__ void __launch_bounds__(kRefThreads, kRefCtasPerSm) count_ref_kernel(S
   for (uint32_t bi = blockIdx.x; bi < a.n_list; bi += gridDim.x) {
     const uint64_t d0 = __ldg(a.range + 2 * (size_t)bi), e1 = __ldg(a.range + 2 * (size_t)bi + 1);
     const uint64_t d1 = e1 & kRangeEndMask, win = e1 >> kRangeWinShift;
-    // descriptors per work unit: ~kSegUnit segments of kSeg windows per unit
     const float avg = (float)win / (float)(d1 > d0 ? d1 - d0 : 1);
-    const float want = (float)(kSegUnit * kSeg) / (avg > 1.0f ? avg : 1.0f);
-    const uint32_t dpc = want >= 32.0f ? 32u : (want <= 1.0f ? 1u : (uint32_t)want);
-    const uint64_t n_units = (d1 - d0 + dpc - 1) / dpc;
     if (tid == 0) {
       s_nd = 0;
       s_abandon = 0;
@@ -111,111 +106,134 @@ __global__ void __launch_bounds__(kRefThreads, kRefCtasPerSm) count_ref_kernel(S
       s_ocur = 0;
     }
     __syncthreads();
-    for (uint64_t u = warp; u < n_units;) {
-      const uint64_t di = d0 + u * dpc + lane;
-      uint64_t pos = 0;
-      uint32_t nw = 0;
-      if (lane < dpc && di < d1) {
-        const uint64_t d = __ldg(a.desc + di);
-        pos = d >> kNwinBits;
-        nw = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
-      }
-      // segments of <= kSeg consecutive windows of one super-mer: a lane takes a segment,
-      // extracts its first k-mer and reverse complement, then rolls both one base per window
-      const uint32_t nseg = (nw + kSeg - 1) / kSeg;
-      uint32_t incl = nseg;
+    // one window per lane: canonical key, probe / claim / verify, then (warp-wide) the list
+    auto process = [&](bool act, uint64_t q) {
+      bool won = false;
+      uint32_t h = 0;
+      if (act) {
+        uint64_t c[W];
+        const bool rc = canon_at<W>(a.codes, q, a.k, canonical, c);
+        const uint64_t hv = key_hash<W>(c);
+        const uint64_t ref = kOcc | ((hv >> 41) << kFpShift) | ((q & kPosMask) << 1) | (rc ? 1ull : 0ull);
+        h = (uint32_t)(((hv & 0xffffffffull) * cap) >> 32);
+        for (;;) {
+          uint64_t v = *(volatile uint64_t*)(s_ref + h);
+          if (v == 0ull) {
+            v = atomicCAS(reinterpret_cast<unsigned long long*>(s_ref + h), 0ull, (unsigned long long)ref);
+            if (v == 0ull) {
+              atomicAdd(s_cnt + h, 1u);
+              won = true;
+              break;
+            }
+          }
+          if ((v >> kFpShift) == (ref >> kFpShift)) {  // same fingerprint: compare the k-mers
+            uint64_t o[W];
+            key_of_ref<W>(a.codes, v, a.k, o);
+            bool eq = true;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= (uint32_t)o) incl += t;
-      }
-      const uint32_t excl = incl - nseg, total = __shfl_sync(kFull, incl, 31);
-      uint32_t n_before = 0;
-      for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t i = base + lane;
-        const bool act = i < total;
-        const uint32_t rel = excl - base;
-        const uint32_t starts = __reduce_or_sync(kFull, (nseg && rel < 32u) ? 1u << rel : 0u);
-        int j = (int)(n_before + __popc(starts & ((2u << lane) - 1u))) - 1;
-        n_before += __popc(starts);
-        if (!act) j = 0;
-        const uint64_t pj = __shfl_sync(kFull, pos, j);
-        const uint32_t ej = __shfl_sync(kFull, excl, j), nwj = __shfl_sync(kFull, nw, j);
-        const uint32_t off = act ? (i - ej) * kSeg : 0u;
-        const uint32_t cnt = act ? min((uint32_t)kSeg, nwj - off) : 0u;
-        const uint32_t steps = __reduce_max_sync(kFull, cnt);
-        const uint64_t q0 = pj + off;
-        uint64_t x[W], r[W];
-        if (cnt) {
-          extract_kmer<W>(a.codes, q0, a.k, x);
-          reverse_complement<W>(x, a.k, r);
+            for (int w = 0; w < W; ++w) eq = eq && o[w] == c[w];
+            if (eq) {
+              atomicAdd(s_cnt + h, 1u);
+              break;
+            }
+          }
+          h = (h + 1 == cap) ? 0u : h + 1;
         }
-        const uint32_t tl = (a.k - 1) & 31;           // the last base's slot in word W-1
-        const uint32_t tail = 2 * a.k - 64 * (W - 1);  // meaningful bits of word W-1
-        const uint64_t tmask = tail < 64 ? ~0ull << (64 - tail) : ~0ull;
-        for (uint32_t t = 0; t < steps; ++t) {
+      }
+      const uint32_t wm = __ballot_sync(kFull, won);
+      if (wm) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(&s_nd, (uint32_t)__popc(wm));
+        b = __shfl_sync(kFull, b, 0);
+        if (won) s_list[b + __popc(wm & ((1u << lane) - 1u))] = (uint16_t)h;
+        if (lane == 0 && b + __popc(wm) > a.max_fill) s_abandon = 1;
+      }
+    };
+    if (avg < (float)kLongSm) {
+      // short super-mers: a unit = dpc consecutive descriptors, lanes = consecutive windows
+      // across them (the window → super-mer map from one OR-reduction per round)
+      const float want = 24.0f / (avg > 1.0f ? avg : 1.0f);
+      const uint32_t dpc = want >= 32.0f ? 32u : (want <= 1.0f ? 1u : (uint32_t)want);
+      const uint64_t n_units = (d1 - d0 + dpc - 1) / dpc;
+      for (uint64_t u = warp; u < n_units;) {
+        const uint64_t di = d0 + u * dpc + lane;
+        uint64_t pos = 0;
+        uint32_t nw = 0;
+        if (lane < dpc && di < d1) {
+          const uint64_t d = __ldg(a.desc + di);
+          pos = d >> kNwinBits;
+          nw = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
+        }
+        uint32_t incl = nw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= (uint32_t)o) incl += t;
+        }
+        const uint32_t excl = incl - nw, total = __shfl_sync(kFull, incl, 31);
+        uint32_t n_before = 0;
+        for (uint32_t base = 0; base < total; base += 32) {
           if (__any_sync(kFull, *(volatile int*)&s_abandon != 0)) break;  // warp-uniform
-          const bool on = t < cnt;
-          bool won = false;
-          uint32_t h = 0;
-          if (on) {
-            const uint64_t q = q0 + t;
-            const bool rc = canonical && key_less<W>(r, x);
-            uint64_t c[W];
-#pragma unroll
-            for (int v = 0; v < W; ++v) c[v] = rc ? r[v] : x[v];
-            const uint64_t hv = key_hash<W>(c);
-            const uint64_t ref = kOcc | ((hv >> 41) << kFpShift) | ((q & kPosMask) << 1) | (rc ? 1ull : 0ull);
-            h = (uint32_t)(((hv & 0xffffffffull) * cap) >> 32);
-            for (;;) {
-              uint64_t v = *(volatile uint64_t*)(s_ref + h);
-              if (v == 0ull) {
-                v = atomicCAS(reinterpret_cast<unsigned long long*>(s_ref + h), 0ull, (unsigned long long)ref);
-                if (v == 0ull) {
-                  atomicAdd(s_cnt + h, 1u);
-                  won = true;
-                  break;
-                }
-              }
-              if ((v >> kFpShift) == (ref >> kFpShift)) {  // same fingerprint: compare the k-mers
-                uint64_t o[W];
-                key_of_ref<W>(a.codes, v, a.k, o);
-                bool eq = true;
-#pragma unroll
-                for (int w = 0; w < W; ++w) eq = eq && o[w] == c[w];
-                if (eq) {
-                  atomicAdd(s_cnt + h, 1u);
-                  break;
-                }
-              }
-              h = (h + 1 == cap) ? 0u : h + 1;
-            }
-            if (t + 1 < cnt) {  // roll: next base enters x at the end, its complement r at the front
-              const uint64_t qn = q + a.k;
-              const uint32_t nb = (uint32_t)(__ldg(a.codes + (qn >> 5)) >> (62 - 2 * (qn & 31))) & 3u;
-#pragma unroll
-              for (int v = 0; v < W - 1; ++v) x[v] = (x[v] << 2) | (x[v + 1] >> 62);
-              x[W - 1] = (x[W - 1] << 2) | ((uint64_t)nb << (62 - 2 * tl));
-#pragma unroll
-              for (int v = W - 1; v > 0; --v) r[v] = (r[v] >> 2) | (r[v - 1] << 62);
-              r[0] = (r[0] >> 2) | ((uint64_t)(3u - nb) << 62);
-              r[W - 1] &= tmask;
-            }
-          }
-          const uint32_t wm = __ballot_sync(kFull, won);
-          if (wm) {
-            uint32_t b = 0;
-            if (lane == 0) b = atomicAdd(&s_nd, (uint32_t)__popc(wm));
-            b = __shfl_sync(kFull, b, 0);
-            if (won) s_list[b + __popc(wm & ((1u << lane) - 1u))] = (uint16_t)h;
-            if (lane == 0 && b + __popc(wm) > a.max_fill) s_abandon = 1;
-          }
+          const uint32_t i = base + lane;
+          const bool act = i < total;
+          const uint32_t rel = excl - base;
+          const uint32_t starts = __reduce_or_sync(kFull, (nw && rel < 32u) ? 1u << rel : 0u);
+          int j = (int)(n_before + __popc(starts & ((2u << lane) - 1u))) - 1;
+          n_before += __popc(starts);
+          if (!act) j = 0;
+          const uint64_t pj = __shfl_sync(kFull, pos, j);
+          const uint32_t ej = __shfl_sync(kFull, excl, j);
+          process(act, pj + (i - ej));
         }
+        uint32_t nu = 0;  // next unit: a dynamic counter per bin (units differ in length)
+        if (lane == 0) nu = atomicAdd(&s_unit, 1u);
+        u = __shfl_sync(kFull, nu, 0);
       }
-      // next unit: a dynamic counter per bin (units differ in length)
-      uint32_t nu = 0;
-      if (lane == 0) nu = atomicAdd(&s_unit, 1u);
-      u = __shfl_sync(kFull, nu, 0);
+    } else {
+      // long super-mers (long reads): a unit = one piece of <= 32 consecutive windows of one
+      // super-mer, numbered over the bin's descriptors (a block scan per batch of kRefThreads
+      // descriptors), so the warps of the CTA end a bin within one round of each other
+      for (uint64_t b0 = d0; b0 < d1; b0 += kRefThreads) {
+        const uint64_t di = b0 + tid;
+        uint64_t dd = 0;
+        uint32_t np = 0;
+        if (di < d1) {
+          dd = __ldg(a.desc + di);
+          np = ((uint32_t)(dd & ((1u << kNwinBits) - 1)) + 1 + 31) / 32;
+        }
+        uint32_t incl = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= (uint32_t)o) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        s_dsc[tid] = dd;
+        __syncthreads();
+        uint32_t wex = 0, tot = 0;
+        for (int q = 0; q < kRefWarps; ++q) {
+          if (q < (int)warp) wex += s_wsum[q];
+          tot += s_wsum[q];
+        }
+        s_pfx[tid] = wex + incl - np;
+        if (tid == 0) s_unit = kRefWarps;
+        __syncthreads();
+        const uint32_t nb = d1 - b0 < (uint64_t)kRefThreads ? (uint32_t)(d1 - b0) : (uint32_t)kRefThreads;
+        for (uint32_t u = warp; u < tot;) {
+          if (__any_sync(kFull, *(volatile int*)&s_abandon != 0)) break;  // warp-uniform
+          uint32_t t = 0;  // last descriptor with s_pfx[t] <= u
+          for (uint32_t step = kRefThreads / 2; step >= 1; step >>= 1)
+            if (t + step < nb && s_pfx[t + step] <= u) t += step;
+          const uint64_t d = s_dsc[t];
+          const uint32_t nw = (uint32_t)(d & ((1u << kNwinBits) - 1)) + 1;
+          const uint32_t off = (u - s_pfx[t]) * 32 + lane;
+          process(off < nw, (d >> kNwinBits) + off);
+          uint32_t nu = 0;
+          if (lane == 0) nu = atomicAdd(&s_unit, 1u);
+          u = __shfl_sync(kFull, nu, 0);
+        }
+        __syncthreads();  // the batch's staging is reused
+      }
     }
     __syncthreads();
     const uint32_t nd = s_nd;
@@ -301,7 +319,7 @@ uint32_t ref_table_slots(size_t smem_per_block) {
   // two CTAs share an SM: each gets half of the SM's shared memory (the opt-in per-block
   // maximum + the 1 KB the runtime reserves per block), minus that reserve and the statics
   const size_t half = (smem_per_block + 1024) / kRefCtasPerSm;
-  const size_t avail = half > 1024 + 256 ? half - 1024 - 256 : 0;
+  const size_t avail = half > 1024 + 6656 ? half - 1024 - 6656 : 0;  // minus the static shared arrays (6.2 KB)
   uint32_t cap = (uint32_t)(avail / 14) & ~31u;
   if (cap > 65504) cap = 65504;  // u16 list entries
   return cap;

@@ -22,6 +22,7 @@ for spec in ${PROF:-c1_supermer:C1:supermer_kernel:3:1 c1_smem:C1:count_smem_ker
   run ncu_$name "timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c $cnt -o gpurun_out/prof_$name -f python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_$name.log 2>&1"
   ncu -i gpurun_out/prof_$name.ncu-rep --page raw --csv > gpurun_out/raw_$name.csv 2>/dev/null
   ncu -i gpurun_out/prof_$name.ncu-rep > gpurun_out/details_$name.txt 2>/dev/null
+  rm -f gpurun_out/prof_$name.ncu-rep  # the merge-back limit is 64 MiB: keep the exports only
 done
 fi
 cat gpurun_out/summary.txt
