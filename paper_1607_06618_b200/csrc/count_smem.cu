@@ -177,9 +177,13 @@ __device__ __forceinline__ uint32_t smem_hash(const uint64_t (&c)[W]) {
 }
 
 
+#ifndef GERBIL_SMEM_RCSTAGE
+#define GERBIL_SMEM_RCSTAGE 0
+#endif
+constexpr bool kRcStage = GERBIL_SMEM_RCSTAGE != 0;  // rc stream staged per chunk (else bit reversal)
 __host__ __device__ constexpr int smem_stage_words(bool pack) { return pack ? 4 : kStageWords; }
 __host__ __device__ constexpr uint32_t smem_overhead(int S) {
-  return 2u * 32u * S * 8u /* forward, double-buffered */ + 32u * S * 8u /* reverse complement */;
+  return 2u * 32u * S * 8u /* forward, double-buffered */ + (kRcStage ? 32u * S * 8u : 0u) /* reverse complement */;
 }
 
 // Per-warp shared memory: [fwd stage 2][32][S] u64 | [rc stage][32][S] u64 |
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
   unsigned char* wbase = s_raw + (size_t)wib * warp_bytes;
   uint64_t* stage = reinterpret_cast<uint64_t*>(wbase);              // [2][32 * S]
   uint64_t* rcs = stage + 2 * 32 * S;                                // [32 * S]
-  unsigned char* tab = reinterpret_cast<unsigned char*>(rcs + 32 * S);
+  unsigned char* tab = reinterpret_cast<unsigned char*>(rcs + (kRcStage ? 32 * S : 0));
   const uint32_t cap = a.cap;
   const uint32_t tail = 2 * a.k - 64 * (W - 1);  // meaningful bits of the last key word
   const uint64_t tmask = tail < 64 ? ~0ull << (64 - tail) : ~0ull;
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
       const uint32_t total = __shfl_sync(kFull, incl, 31);
       const uint32_t stage_mask = __ballot_sync(kFull, staged);
       // reverse-complement stream of every staged super-mer: rc base t = comp(fwd base o+L-1-t)
-      const bool rcst = a.canonical && !(a.dbg & 1u);
+      const bool rcst = kRcStage && a.canonical && !(a.dbg & 1u);
       if (rcst && staged && nw) {
         const uint64_t* f = stg + lane * S;
         uint64_t* r = rcs + lane * S;
@@ -324,6 +328,13 @@ __global__ void __launch_bounds__(kSmemMaxWarps * 32, 1) count_smem_kernel(SmemC
           if (rcst) {  // warp-uniform
             uint64_t r[W];
             extract_fast<W>(rcs + j * S, act ? Lj - q - a.k : 0u, tmask, r);
+            if (key_less<W>(r, c)) {
+#pragma unroll
+              for (int v = 0; v < W; ++v) c[v] = r[v];
+            }
+          } else if (a.canonical) {  // no rc stage: reverse complement by bit reversal
+            uint64_t r[W];
+            reverse_complement<W>(c, a.k, r);
             if (key_less<W>(r, c)) {
 #pragma unroll
               for (int v = 0; v < W; ++v) c[v] = r[v];
