@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(kRefThreads, kRefCtasPerSm) count_ref_kernel(S
         const uint64_t hv = key_hash<W>(c);
         const uint64_t ref = kOcc | ((hv >> 41) << kFpShift) | ((q & kPosMask) << 1) | (rc ? 1ull : 0ull);
         h = (uint32_t)(((hv & 0xffffffffull) * cap) >> 32);
-        for (;;) {
+        // a bin too large for one table is counted in `parts` passes, each taking the k-mers of
+        // one hash class (every occurrence of a k-mer is in the same class)
+        const bool mine = a.parts <= 1 || (uint32_t)((hv >> 32) % a.parts) == a.part;
+        for (; mine;) {
           uint64_t v = *(volatile uint64_t*)(s_ref + h);
           if (v == 0ull) {
             v = atomicCAS(reinterpret_cast<unsigned long long*>(s_ref + h), 0ull, (unsigned long long)ref);

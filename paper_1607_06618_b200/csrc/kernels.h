@@ -205,6 +205,7 @@ struct SmemCountArgs {
   uint32_t dbg;                      // diagnostics: 1 = no rc stage, 2 = no window map, 8 = full-size tables
   int32_t warps;                     // warps per CTA (0 = smem_count_warps(k)); cap must match; -1 = the
                                      // CTA-wide reference tables of count_ref.cu (any W)
+  uint32_t parts, part;              // count_ref: only k-mers with (hash >> 32) % parts == part (0/1 = all)
 };
 // Table slots a bin of `win` windows gets (count_smem_kernel): windows * 1.25 + 32, rounded up to 32,
 // capped at the warp's table (cap).

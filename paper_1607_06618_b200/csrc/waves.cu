@@ -616,6 +616,75 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       trace("smem tier 2 done (synced)");
     }
   }
+  // Long keys (reference tables in tier 1): a bin too large for one CTA table is counted in P
+  // passes over its super-mers, pass p keeping the k-mers whose hash class is p (distinct k-mers
+  // spread evenly over the classes: P = 1.5 x windows / max_fill (distinct <= windows) leaves each
+  // pass at most 2/3 of max_fill on average — an overflow would need a deviation of dozens of
+  // standard deviations over thousands of keys; it fails the call loudly rather than recount a bin
+  // whose other classes are already output). Bins beyond 128 classes stay with the wave tables.
+  if (!rest.empty() && ref_tier1(ctx, k) && ctx->cfg.count_mode != 1) {
+    std::vector<RestBin> keep;
+    std::vector<std::vector<RestBin>> by_p(7);  // P = 2, 4, ..., 128
+    for (const RestBin& rb : rest) {
+      const uint64_t want = (3 * rb.win + 2 * (uint64_t)max_fill - 1) / (2 * (uint64_t)std::max<uint32_t>(max_fill, 1));
+      int e = 1;
+      while (e < 7 && (1ull << e) < want) ++e;
+      if ((1ull << e) >= want && rb.win < (1ull << 24)) by_p[e - 1].push_back(rb);
+      else keep.push_back(rb);
+    }
+    for (int e = 1; e <= 7; ++e) {
+      const std::vector<RestBin>& L = by_p[e - 1];
+      if (L.empty()) continue;
+      const uint32_t P = 1u << e;
+      uint64_t wsum = 0;
+      CK(ctx->h_rng.ensure(L.size() * 16));
+      unsigned long long* r2 = ctx->h_rng.as<unsigned long long>();
+      for (size_t i = 0; i < L.size(); ++i) {
+        r2[2 * i] = L[i].d0;
+        r2[2 * i + 1] = L[i].d1 | (L[i].win << kRangeWinShift);
+        wsum += L[i].win;
+      }
+      const uint64_t out2 = pre.out_n + wsum;
+      CK(ensure_keep(ctx->out_keys, out2 * W * 8, pre.out_n * W * 8, ctx->stream));
+      CK(ensure_keep(ctx->out_counts, out2 * 4, pre.out_n * 4, ctx->stream));
+      CK(ctx->smem_range.ensure(L.size() * 16));
+      CK(ctx->smem_failed.ensure(L.size() * 16 + 16));
+      CK(cudaMemcpyAsync(ctx->smem_range.p, r2, L.size() * 16, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemsetAsync(&dc->read_work, 0, 8, ctx->stream));
+      SmemCountArgs a3 = a;
+      a3.range = ctx->smem_range.as<unsigned long long>();
+      a3.n_list = (uint32_t)L.size();
+      a3.out_keys = ctx->out_keys.as<uint64_t>();
+      a3.out_counts = ctx->out_counts.as<uint32_t>();
+      a3.out_cap = out2;
+      a3.failed = ctx->smem_failed.as<unsigned long long>();
+      a3.parts = P;
+      for (uint32_t q = 0; q < P; ++q) {
+        a3.part = q;
+        if (streaming) {
+          CK(cudaStreamSynchronize(ctx->pcie_stream));
+          rec_done = 0;
+          CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+          CK(ctx->rec_stage2.ensure(std::max<uint64_t>(wsum, 1) * rec_max + 64));
+          CKS(stream_slices(a3, (uint32_t)L.size(), 1));
+        } else {
+          Timer tm(ctx, K_SMEM);
+          CK(launch_count_smem(a3, ctx->sms, ctx->stream));
+        }
+      }
+      CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (hc.read_work) return fail(ctx, GERBIL_E_INTERNAL, "hash-class pass overflowed a reference table");
+      if (hc.out_n > out2) return fail(ctx, GERBIL_E_INTERNAL, "hash-class pass result bound violated");
+      pre.out_n = hc.out_n;
+      pre.sum_counts = hc.sum_counts;
+      pre.distinct = hc.distinct;
+      ctx->stats.smem_bins += L.size();
+      smem_windows += wsum;
+    }
+    rest.swap(keep);
+    trace("hash-class passes done (synced)");
+  }
   ctx->stats.smem_windows += smem_windows;
   const double smem_obs = smem_windows ? (double)pre.distinct / (double)smem_windows : 0.0;
   gerbil_status st = GERBIL_OK;
