@@ -183,7 +183,7 @@ cudaError_t launch_count_wide(const CountArgs& a, int sms, cudaStream_t s);  // 
 // count_smem.cu: steps (d)+(e) for bins whose distinct k-mers fit one warp's
 // shared-memory table (one warp per bin, warp-synchronous inserts, in-place
 // compaction). Abandoned bins (distinct > max_fill) are listed in `failed`.
-constexpr int kSmemMaxWarps = 16;
+constexpr int kSmemMaxWarps = 24;
 constexpr int kRangeWinShift = 40;  // bin windows (clamped to 2^24 - 1) above the end descriptor index
 constexpr unsigned long long kRangeEndMask = (1ull << kRangeWinShift) - 1;
 struct SmemCountArgs {
