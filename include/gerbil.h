@@ -303,8 +303,16 @@ gerbil_status gerbil_count_text(gerbil_ctx* ctx, const char* text, uint64_t len,
  * call or any other error ends the job. The histogram is
  * the same as one gerbil_count over the concatenated batches. No device
  * result set remains (gerbil_fetch → GERBIL_E_STATE); stats describe the whole
- * job. One rank only; the DFP ordering is refused (its table is per batch).
- * GERBIL_E_STATE when called out of order. */
+ * job. world > 1: each rank spills its own batches and gerbil_spill_finish is
+ * collective (every rank calls it): the bins are split into contiguous ranges
+ * of about equal global windows, rank d counts range d (its records: the k-mers
+ * of those bins, with counts over every rank's batches), the groups move in
+ * rounds of one grouped all-to-all each; the job parameters (bins, k, m,
+ * ordering, disable_normalization) must agree (else GERBIL_E_USAGE), and the
+ * job is kept on every rank unless every rank's records fit (then every rank
+ * returns GERBIL_E_USAGE with its own *n_bytes, and all call again).
+ * The DFP ordering is refused (its table is per batch); force_exchange is
+ * refused. GERBIL_E_STATE when called out of order. */
 gerbil_status gerbil_spill_begin(gerbil_ctx* ctx, uint32_t k, uint32_t m);
 gerbil_status gerbil_spill_add(gerbil_ctx* ctx, const uint64_t* codes, const uint64_t* nmask,
                                const uint64_t* read_start, uint64_t n_reads);

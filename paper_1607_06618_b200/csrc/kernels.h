@@ -94,6 +94,7 @@ struct ScatterArgs {
 };
 constexpr int kDescPackShift = 54;
 cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t s);
+cudaError_t launch_rebase_desc(uint64_t* desc, uint64_t n, uint64_t pos_add, int sms, cudaStream_t s);
 // Second level of a two-level scatter: descriptors already grouped by bin >> shift
 // (group g = [off[g << shift], off[min((g + 1) << shift, n_bins)]) of desc_in/bin_in)
 // are regrouped by bin inside each group with shared-memory cursors.

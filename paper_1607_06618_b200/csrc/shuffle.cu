@@ -653,6 +653,23 @@ cudaError_t launch_pack(const PackArgs& a, int sms, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void rebase_desc_kernel(uint64_t* desc, uint64_t n, uint64_t pos_add) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    desc[i] += pos_add << kNwinBits;
+}
+}  // namespace
+
+// In-place position rebase of n descriptors (pos += pos_add mod 2^64 >> kNwinBits): spilled
+// chunks of several batches placed side by side in one send segment (spill.cu, world > 1).
+cudaError_t launch_rebase_desc(uint64_t* desc, uint64_t n, uint64_t pos_add, int sms, cudaStream_t st) {
+  if (n == 0 || pos_add == 0) return cudaSuccess;
+  const uint64_t want = (n + 255) / 256, cap = (uint64_t)sms * 8;
+  const uint64_t blocks = want < cap ? want : cap;
+  rebase_desc_kernel<<<(unsigned)blocks, 256, 0, st>>>(desc, n, pos_add);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(const ScatterArgs& a, int sms, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
   const uint32_t nb = ((a.n_bins - 1) >> a.bin_shift) + 1;  // groups the kernel sees

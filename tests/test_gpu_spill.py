@@ -129,3 +129,65 @@ def test_spill_usage_errors(G):
         with pytest.raises(G.GerbilError) as e:
             g.spill_begin(28, 7)
         assert e.value.status == G.E_USAGE
+
+
+# ---- world > 1: every rank spills its own batches; bin ranges are counted by their owners ----
+def _spill_ranks(G, P, texts_per_rank, k, m, min_count, uid, **kw):
+    import threading
+
+    results, errors = [None] * P, []
+
+    def rank(r):
+        try:
+            with G.Gerbil(rank=r, world=P, unique_id=uid, comm_backend=1, **kw) as g:
+                packs = [G.pack_reads(t) for t in texts_per_rank[r]]
+                g.spill_begin(k, m)
+                for p in packs:
+                    g.spill_add(p.codes, p.nmask, p.read_start, p.n_reads)
+                try:  # sizing call: collective, keeps the job on every rank
+                    g.spill_finish(min_count, out=None)
+                    need = 0
+                except G.GerbilError as e:
+                    need = e.needed_bytes
+                out = _pinned(need)
+                n = g.spill_finish(min_count, out=out)
+                results[r] = (out[:n].tobytes(), g.stats())
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(P)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    return results
+
+
+@pytest.mark.parametrize("P,k,group_bytes", [(2, 40, "0"), (2, 65, "120000"), (3, 28, "90000"), (4, 100, "0")])
+def test_spill_ranks_match_oracle(G, P, k, group_bytes, monkeypatch):
+    if group_bytes != "0":
+        monkeypatch.setenv("GERBIL_SPILL_GROUP_BYTES", group_bytes)  # several rounds of groups
+    texts = _batches(200 + k, n=2 * P, reads=1200)
+    per_rank = [texts[r::P] for r in range(P)]  # rank r spills batches r, r + P, ...
+    ref = oracle.count(b"".join(texts), k)
+    want = sorted(oracle.encode_entry(x, c) for x, c in zip(ref.kmers, ref.counts))
+    res = _spill_ranks(G, P, per_rank, k, 7, 1, bytes([40 + P + k % 50]) * 128, n_bins=64)
+    got = sorted(r for buf, _ in res for r in _records(buf, k))
+    assert got == want  # every k-mer exactly once, on its owner, with the global count
+    sts = [s for _, s in res]
+    assert sum(s["count_sum"] for s in sts) == ref.windows == sum(s["valid_windows"] for s in sts)
+    assert sum(s["distinct"] for s in sts) == ref.distinct
+    assert all(s["count_sum"] == s["owned_windows"] for s in sts)
+    assert all(s["bytes_recv"] > 0 for s in sts)
+
+
+def test_spill_ranks_min_count_and_empty_rank(G):
+    # rank 1 spills nothing at all; min_count 2
+    P, k = 2, 40
+    texts = _batches(31, n=3, reads=1000)
+    ref = oracle.count(b"".join(texts), k, 2)
+    want = sorted(oracle.encode_entry(x, c) for x, c in zip(ref.kmers, ref.counts))
+    res = _spill_ranks(G, P, [texts, []], k, 7, 2, b"\x5a" * 128, n_bins=32)
+    assert sorted(r for buf, _ in res for r in _records(buf, k)) == want
+    assert res[1][1]["valid_windows"] == 0 and res[1][1]["count_sum"] > 0
