@@ -332,6 +332,10 @@ inline bool ref_tier1(const gerbil_ctx* ctx, uint32_t k) {
   (void)ctx;
   return key_words(k) >= 4;
 }
+// CTAs per SM of the first reference-table tier: 2 = two bins in flight per SM on half tables
+// (a bin's warps wait at its barriers while the other bin's keep the SM busy; bins that do not fit
+// go to the full-table second tier), 1 = one bin per SM (GERBIL_REF_CTAS overrides)
+int ref_tier1_ctas();
 // from this many bins up, a single rank plans steps (c)-(e) on the device
 constexpr uint32_t kDevicePlanBins = 1u << 16;
 gerbil_status count_local_device_plan(gerbil_ctx* ctx, const uint64_t* codes, uint64_t n_sm, uint32_t B,

@@ -227,7 +227,7 @@ uint32_t smem_table_slots(uint32_t k, size_t smem_per_block, int warps = 0);  //
 cudaError_t launch_count_smem(const SmemCountArgs& a, int sms, cudaStream_t s);  // W >= 4: count_ref
 // count_ref.cu (W >= 4): a.cap = slots of the CTA-wide table of occurrence references
 size_t ref_table_bytes(uint32_t cap);
-uint32_t ref_table_slots(size_t smem_per_block);
+uint32_t ref_table_slots(size_t smem_per_block, int ctas_per_sm = 1);  // 2: two 256-thread CTAs per SM (a.warps = -2)
 uint32_t ref_max_fill(uint32_t cap);
 cudaError_t launch_count_ref(const SmemCountArgs& a, int sms, cudaStream_t s);
 struct PlanBinsArgs {

@@ -33,6 +33,8 @@
 //   5. bin = fastrange(fmix32(μ), B); descriptors are appended with one global
 //      atomic per tile; per-bin counts accumulate in smem and are flushed once
 //      per persistent CTA.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "ordering.cuh"
@@ -109,7 +111,11 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #ifndef GERBIL_SM_MINB
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
-template <uint32_t ORD, int KMAX, uint32_t MT>  // MT: m fixed at compile time (0 = runtime a.m)
+// A8 (w = k-m+1 <= 65, the KMAX = 200 geometry): key blocks of 8 aligned with the thread's 8
+// windows, so a window's minimum is the suffix of the thread's OWN block (registers) + whole
+// blocks + the prefix of one later block (shared memory); the w-1 keys past the tile's 1024
+// positions are computed one per lane by warps 0-1 (prefix minima by 8-lane shuffle scans).
+template <uint32_t ORD, int KMAX, uint32_t MT, bool A8 = false>  // MT: m fixed at compile time (0 = runtime a.m)
 __global__ void __launch_bounds__(kThreads, GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,
                 int hist_smem) {
@@ -122,7 +128,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
   __shared__ uint32_t s_key[kKeyLen];    // c_j
   __shared__ uint32_t s_pre[kKeyLen];    // min over c[8b .. j] (j in block b)
   __shared__ uint32_t s_suf[kKeyLen];    // min over c[j .. 8b+7]
-  __shared__ uint32_t s_blk[kKeyBlocks]; // min over block b
+  __shared__ uint32_t s_blk[kKeyBlocks + 8]; // min over block b (A8: 8 more blocks past the tile)
   __shared__ uint32_t s_brk[kSTile / 32 + 1];
   __shared__ uint32_t s_last[kThreads];  // μ of window 8t+7, or ~0 if invalid
   __shared__ uint16_t s_sp[kSTile];      // the tile's super-mer start positions
@@ -188,70 +194,142 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
     stage_store(staged);
     __syncthreads();
     staged = stage_load(tile + gridDim.x);  // in flight while this tile is processed
-    // 2. rolling strand-symmetric m-mer keys of key block t (kKB keys, exactly
-    //    one block per thread), block prefix/suffix minima
-    {
-      const uint32_t j0 = kKB * tid;
-      // initial m-mer at j0
-      const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
-      const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
-      // the block's bases j0 .. j0+kKB-1+m-1 (<= 26) all sit in v; R = reverse complement of v's
-      // 32 bases, so the m-mer at i is bits [64-2(i+m), 64-2i) of v and its reverse complement
-      // bits [2i, 2i+2m) of R — independent extractions (no rolling dependency chain)
-      const uint64_t R = rev_pairs(~v);
-      uint32_t c[kKB];
-#pragma unroll
-      for (int i = 0; i < kKB; ++i) {
-        const uint32_t f = (uint32_t)(v >> (64 - 2 * (i + m))) & mmask;
-        const uint32_t rc = (uint32_t)(R >> (2 * i)) & mmask;
-        const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
-        c[i] = kf < kr ? kf : kr;
-      }
-      uint32_t pre = 0xffffffffu;
-#pragma unroll
-      for (int i = 0; i < kKB; ++i) {
-        pre = min(pre, c[i]);
-        if (w < 2 * kKB) s_key[j0 + i] = c[i];
-        s_pre[j0 + i] = pre;
-      }
-      uint32_t suf = 0xffffffffu;
-#pragma unroll
-      for (int i = kKB - 1; i >= 0; --i) {
-        suf = min(suf, c[i]);
-        s_suf[j0 + i] = suf;
-      }
-      s_blk[tid] = suf;
-    }
-    __syncthreads();
-    // 3. minimizers and validity of windows 8t .. 8t+7
     uint32_t mu[kPer];
-    uint32_t vmask = 0;
-    {
-      const uint32_t s0 = tid * kPer;
-      if (w >= 2 * kKB) {
-        // window [s, e] (e = s+w-1) = suffix of block s/kKB, the whole blocks in
-        // between, prefix of block e/kKB. The 8 windows share every whole block
-        // strictly between bsL = (s0+7)/kKB and beF = (s0+w-1)/kKB.
-        const uint32_t bsL = (s0 + kPer - 1) / kKB, beF = (s0 + w - 1) / kKB;
-        uint32_t mid = 0xffffffffu;
-        for (uint32_t b = bsL + 1; b < beF; ++b) mid = min(mid, s_blk[b]);
-        const uint32_t xa = s_blk[bsL], xb = s_blk[beF];
+    if constexpr (A8) {
+      // 2'. keys of the thread's own block 8t .. 8t+7 (one u64 of bases, independent extractions)
+      static_assert(kPer == 8 && KMAX <= 200, "aligned blocks of 8");
+      const uint32_t j0 = kPer * tid;
+      uint32_t c[kPer];
+      {
+        const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
+        const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
+        const uint64_t R = rev_pairs(~v);
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
-          const uint32_t s = s0 + i, e = s + w - 1;
-          uint32_t m2 = mid;
-          if (s / kKB < bsL) m2 = min(m2, xa);
-          if (e / kKB > beF) m2 = min(m2, xb);
-          mu[i] = min(min(s_suf[s], s_pre[e]), m2);
+          const uint32_t f = (uint32_t)(v >> (64 - 2 * (i + m))) & mmask;
+          const uint32_t rc = (uint32_t)(R >> (2 * i)) & mmask;
+          const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
+          c[i] = kf < kr ? kf : kr;
         }
-      } else {
+        uint32_t pre = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          pre = min(pre, c[i]);
+          s_pre[j0 + i] = pre;
+        }
+        s_blk[tid] = pre;
+      }
+      // the keys past the tile (positions 1024 .. 1024+w-2 <= 1087): one per lane of warps 0-1
+      if (tid < 64) {
+        const uint32_t j = kSTile + tid, wi = j >> 5, sh = (j & 31) * 2;
+        const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
+        const uint32_t f = (uint32_t)(v >> (64 - 2 * m)) & mmask;
+        const uint32_t rc = (uint32_t)(rev_pairs(~v) & mmask);
+        const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
+        uint32_t x = kf < kr ? kf : kr;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {  // prefix minima within blocks of 8 lanes
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o, 8);
+          if ((lane & 7) >= (uint32_t)o) x = min(x, y);
+        }
+        s_pre[j] = x;
+        if ((lane & 7) == 7) s_blk[j >> 3] = x;
+      }
+      __syncthreads();
+      // 3'. minimizers of windows 8t+i = min(suffix of c from i, whole blocks, prefix at the end)
+      uint32_t suf[kPer];
+      suf[kPer - 1] = c[kPer - 1];
+#pragma unroll
+      for (int i = kPer - 2; i >= 0; --i) suf[i] = min(c[i], suf[i + 1]);
+      if (w <= kPer) {  // short windows may end inside the own block
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
           uint32_t x = 0xffffffffu;
-          for (uint32_t j = s0 + i; j < s0 + i + w; ++j) x = min(x, s_key[j]);
+#pragma unroll
+          for (int j = i; j < kPer; ++j)
+            if ((uint32_t)(j - i) < w) x = min(x, c[j]);
+          if ((uint32_t)i + w > (uint32_t)kPer) x = min(x, s_pre[j0 + i + w - 1]);
           mu[i] = x;
         }
+      } else {
+        const uint32_t qa = (w - 1) >> 3, ra = (w - 1) & 7;  // window 0 ends at block t+qa, offset ra
+        uint32_t midA = 0xffffffffu;
+        for (uint32_t b = 1; b < qa; ++b) midA = min(midA, s_blk[tid + b]);
+        const uint32_t midB = min(midA, s_blk[tid + qa]);  // windows ending in block t+qa+1
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t mid = (uint32_t)i + ra >= (uint32_t)kPer ? midB : midA;
+          mu[i] = min(min(suf[i], mid), s_pre[j0 + i + w - 1]);
+        }
       }
+    } else {
+      // 2. rolling strand-symmetric m-mer keys of key block t (kKB keys, exactly
+      //    one block per thread), block prefix/suffix minima
+      {
+        const uint32_t j0 = kKB * tid;
+        // initial m-mer at j0
+        const uint32_t wi = j0 >> 5, sh = (j0 & 31) * 2;
+        const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
+        // the block's bases j0 .. j0+kKB-1+m-1 (<= 26) all sit in v; R = reverse complement of v's
+        // 32 bases, so the m-mer at i is bits [64-2(i+m), 64-2i) of v and its reverse complement
+        // bits [2i, 2i+2m) of R — independent extractions (no rolling dependency chain)
+        const uint64_t R = rev_pairs(~v);
+        uint32_t c[kKB];
+  #pragma unroll
+        for (int i = 0; i < kKB; ++i) {
+          const uint32_t f = (uint32_t)(v >> (64 - 2 * (i + m))) & mmask;
+          const uint32_t rc = (uint32_t)(R >> (2 * i)) & mmask;
+          const uint32_t kf = order_key<ORD>(f, ord), kr = order_key<ORD>(rc, ord);
+          c[i] = kf < kr ? kf : kr;
+        }
+        uint32_t pre = 0xffffffffu;
+  #pragma unroll
+        for (int i = 0; i < kKB; ++i) {
+          pre = min(pre, c[i]);
+          if (w < 2 * kKB) s_key[j0 + i] = c[i];
+          s_pre[j0 + i] = pre;
+        }
+        uint32_t suf = 0xffffffffu;
+  #pragma unroll
+        for (int i = kKB - 1; i >= 0; --i) {
+          suf = min(suf, c[i]);
+          s_suf[j0 + i] = suf;
+        }
+        s_blk[tid] = suf;
+      }
+      __syncthreads();
+      // 3. minimizers and validity of windows 8t .. 8t+7
+      {
+        const uint32_t s0 = tid * kPer;
+        if (w >= 2 * kKB) {
+          // window [s, e] (e = s+w-1) = suffix of block s/kKB, the whole blocks in
+          // between, prefix of block e/kKB. The 8 windows share every whole block
+          // strictly between bsL = (s0+7)/kKB and beF = (s0+w-1)/kKB.
+          const uint32_t bsL = (s0 + kPer - 1) / kKB, beF = (s0 + w - 1) / kKB;
+          uint32_t mid = 0xffffffffu;
+          for (uint32_t b = bsL + 1; b < beF; ++b) mid = min(mid, s_blk[b]);
+          const uint32_t xa = s_blk[bsL], xb = s_blk[beF];
+  #pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const uint32_t s = s0 + i, e = s + w - 1;
+            uint32_t m2 = mid;
+            if (s / kKB < bsL) m2 = min(m2, xa);
+            if (e / kKB > beF) m2 = min(m2, xb);
+            mu[i] = min(min(s_suf[s], s_pre[e]), m2);
+          }
+        } else {
+  #pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            uint32_t x = 0xffffffffu;
+            for (uint32_t j = s0 + i; j < s0 + i + w; ++j) x = min(x, s_key[j]);
+            mu[i] = x;
+          }
+        }
+      }
+    }
+    uint32_t vmask = 0;
+    {
+      const uint32_t s0 = tid * kPer;
       // window s0+i is valid iff the next X position >= s0+i lies beyond s0+i+k-2
       // and base s0+i+k-1 is not N. x8 = X bits of the thread's own 8 positions
       // (s0 is 8-aligned), ns2 = next X at or after s0+8, n8 = N bits of the
@@ -326,12 +404,13 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
     //    threads emit them together (full lanes, coalesced descriptor writes)
     {
       uint32_t o = s_warp[warp] + (incl - nst);
-      while (smask) {
-        const int i = __ffs(smask) - 1;
-        smask &= smask - 1;
-        s_sp[o] = (uint16_t)(tid * kPer + i);
-        s_smu[o] = mu[i];
-        ++o;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {  // unrolled: mu stays in registers (no local-memory array)
+        if ((smask >> i) & 1u) {
+          s_sp[o] = (uint16_t)(tid * kPer + i);
+          s_smu[o] = mu[i];
+          ++o;
+        }
       }
     }
     __syncthreads();
@@ -412,6 +491,15 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
 #define GERBIL_SM_ORD(O) \
   case O: return wide ? go(supermer_kernel<O, kMaxKAll, 0>) : go(supermer_kernel<O, kMaxKSmall, 0>)
   // the default ordering with the common minimizer lengths: shifts and masks as constants
+  static const bool a8_on = [] {
+    const char* e = getenv("GERBIL_SM_A8");
+    return !(e && atoi(e) == 0);
+  }();
+  if (a.ordering == kOrdKMC2 && !wide && a.k - a.m + 1 <= 65 && a8_on) {
+    if (a.m == 15) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 15, true>);
+    if (a.m == 11) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 11, true>);
+    if (a.m == 7) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 7, true>);
+  }
   if (a.ordering == kOrdKMC2 && !wide) {
     if (a.m == 15) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 15>);
     if (a.m == 11) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 11>);

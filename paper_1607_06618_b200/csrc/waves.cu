@@ -347,6 +347,14 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
   }
 }
 
+int ref_tier1_ctas() {
+  static const int c = [] {
+    const char* e = getenv("GERBIL_REF_CTAS");
+    return e && atoi(e) == 1 ? 1 : 2;
+  }();
+  return c;
+}
+
 // Shared-memory table slots per warp for this k (0 = shared-memory path off).
 uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
   if (ctx->cfg.count_mode == 1) return 0;
@@ -357,7 +365,7 @@ uint32_t smem_slots_for(gerbil_ctx* ctx, uint32_t k) {
   }
   // W >= 4, or mostly distinct k-mers: one CTA-wide table of occurrence references per bin
   // (count_ref.cu); else per-warp tables of whole keys (count_smem.cu)
-  const uint32_t cap = ref_tier1(ctx, k) ? ref_table_slots((size_t)ctx->smem_optin - 1024)
+  const uint32_t cap = ref_tier1(ctx, k) ? ref_table_slots((size_t)ctx->smem_optin - 1024, ref_tier1_ctas())
                                          : smem_table_slots(k, (size_t)ctx->smem_optin - 1024);
   return cap >= 128 ? cap : 0;
 }
@@ -409,7 +417,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   a.canonical = ctx->cfg.disable_normalization ? 0u : 1u;
   a.cap = cap;
   a.max_fill = max_fill;
-  a.warps = ref_tier1(ctx, k) ? -1 : 0;  // -1: CTA-wide reference tables
+  a.warps = ref_tier1(ctx, k) ? -ref_tier1_ctas() : 0;  // -1 / -2: CTA-wide reference tables (1 / 2 per SM)
   a.out_n = &dc->out_n;
   a.sum_counts = &dc->sum_counts;
   a.distinct = &dc->distinct;
@@ -532,6 +540,50 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   ctx->stats.smem_bins += n;
   ctx->stats.smem_failed += n_failed;
   uint64_t smem_windows = elig_windows - std::min(elig_windows, failed_windows);
+  // A later pass (tier 2, hash-class passes) appends after base.out_n: the result buffer grows by
+  // at most `bound` entries but never past the result budget (with min_count > 1 on singleton-rich
+  // input the bound is far larger than what is kept); if the kept results do not fit, the pass is
+  // rerun once with the exact size after the counters are restored to `base`.
+  auto run_pass = [&](const Preset& base, uint64_t bound, auto&& issue) -> gerbil_status {
+    // entries the buffers could hold: their present size plus 85 % of the free device memory
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      fr = 0;
+    }
+    const uint64_t room = (uint64_t)((fr * 0.85 + (double)ctx->out_keys.bytes + (double)ctx->out_counts.bytes) /
+                                     (W * 8.0 + 4.0));
+    const uint64_t grow = std::max<uint64_t>(room > base.out_n ? room - base.out_n : 0,
+                                             std::max<uint64_t>(result_budget_entries(ctx, W, 5), 1));
+    uint64_t cap_n = base.out_n + std::min<uint64_t>(std::max<uint64_t>(bound, 1), grow);
+    const uint64_t host_start = host_off;
+    for (int attempt = 0;; ++attempt) {
+      CK(ensure_keep(ctx->out_keys, cap_n * W * 8, base.out_n * W * 8, ctx->stream));
+      CK(ensure_keep(ctx->out_counts, cap_n * 4, base.out_n * 4, ctx->stream));
+      if (streaming) {  // the previous pass's records are copied out: this pass starts a fresh staging area
+        CK(cudaStreamSynchronize(ctx->pcie_stream));
+        rec_done = 0;
+        CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
+        CK(ctx->rec_stage2.ensure((cap_n - base.out_n) * rec_max + 64));
+      }
+      CKS(issue(ctx->out_keys.as<uint64_t>(), ctx->out_counts.as<uint32_t>(), cap_n));
+      CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (hc.out_n > base.out_n + bound) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+      if (hc.out_n <= cap_n) return GERBIL_OK;
+      if (attempt > 0) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory pass: result size changed on rerun");
+      cap_n = hc.out_n;  // exact: the rerun keeps the same k-mers
+      host_off = host_start;
+      Counters r = hc;
+      r.ovf_n = 0;
+      r.read_work = 0;
+      r.out_n = base.out_n;
+      r.sum_counts = base.sum_counts;
+      r.distinct = base.distinct;
+      CK(cudaMemcpyAsync(dc, &r, sizeof(Counters), cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  };
   // Tier 2 (W <= 3): bins too large for the per-warp tables get a second launch — with mostly
   // repeated k-mers (rho < 0.35, e.g. C1) on half as many warps (twice the slots per warp),
   // with mostly distinct ones (C2/C3 shards) on one CTA-wide table of occurrence references per
@@ -541,11 +593,15 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   const bool tier2_ref = !tier1_ref && W <= 3 && ctx->rho > 0.35;
   const int w1 = a.warps > 0 ? a.warps : smem_count_warps(k);
   const int w2n = std::max(1, w1 / 2);
-  const uint32_t cap2 = tier1_ref ? 0u
-                        : tier2_ref ? ref_table_slots((size_t)ctx->smem_optin - 1024)
+  // the full-size reference table: tier 2 after half tables in tier 1 (W >= 4, two CTAs per SM),
+  // tier 2 for mostly distinct short keys, and the hash-class passes below
+  const uint32_t cap_full = ref_table_slots((size_t)ctx->smem_optin - 1024, 1);
+  const bool ref2 = tier2_ref || (tier1_ref && a.warps == -2);
+  const uint32_t cap2 = ref2 ? cap_full
+                        : tier1_ref ? 0u
                                     : (w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u);
   if (!rest.empty() && cap2 > cap) {
-    const uint32_t mf2 = tier2_ref ? ref_max_fill(cap2) : cap2 - std::max<uint32_t>(64u, cap2 / 4);
+    const uint32_t mf2 = ref2 ? ref_max_fill(cap2) : cap2 - std::max<uint32_t>(64u, cap2 / 4);
     const uint64_t thr2 = smem_window_threshold(ctx, mf2);
     std::vector<RestBin> keep;
     uint64_t n2 = 0, w2 = 0, ob2 = 0;
@@ -563,9 +619,6 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       }
     }
     if (n2) {
-      const uint64_t out2 = pre.out_n + ob2;
-      CK(ensure_keep(ctx->out_keys, out2 * W * 8, pre.out_n * W * 8, ctx->stream));
-      CK(ensure_keep(ctx->out_counts, out2 * 4, pre.out_n * 4, ctx->stream));
       CK(ctx->smem_range.ensure(n2 * 16));
       CK(ctx->smem_failed.ensure(n2 * 16 + 16));
       CK(cudaMemcpyAsync(ctx->smem_range.p, r2, n2 * 16, cudaMemcpyHostToDevice, ctx->stream));
@@ -575,24 +628,20 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       a2.n_list = (uint32_t)n2;
       a2.cap = cap2;
       a2.max_fill = mf2;
-      a2.warps = tier2_ref ? -1 : w2n;  // -1: the CTA-wide reference tables
-      a2.out_keys = ctx->out_keys.as<uint64_t>();
-      a2.out_counts = ctx->out_counts.as<uint32_t>();
-      a2.out_cap = out2;
+      a2.warps = ref2 ? -1 : w2n;  // -1: the CTA-wide reference tables, one per SM
       a2.failed = ctx->smem_failed.as<unsigned long long>();
-      if (streaming) {  // tier 1's records are copied out: tier 2's start a fresh staging area
-        CK(cudaStreamSynchronize(ctx->pcie_stream));
-        rec_done = 0;
-        CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
-        CK(ctx->rec_stage2.ensure(std::max<uint64_t>(ob2, 1) * rec_max + 64));
-        CKS(stream_slices(a2, (uint32_t)n2, 1));
-      } else {
-        Timer tm(ctx, K_SMEM);
-        CK(launch_count_smem(a2, ctx->sms, ctx->stream));
-      }
-      CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
-      CK(cudaStreamSynchronize(ctx->stream));
-      if (hc.out_n > out2) return fail(ctx, GERBIL_E_INTERNAL, "shared-memory result bound violated");
+      CKS(run_pass(pre, ob2, [&](uint64_t* ok, uint32_t* oc, uint64_t cap_n) -> gerbil_status {
+        a2.out_keys = ok;
+        a2.out_counts = oc;
+        a2.out_cap = cap_n;
+        if (streaming) {
+          CKS(stream_slices(a2, (uint32_t)n2, 1));
+        } else {
+          Timer tm(ctx, K_SMEM);
+          CK(launch_count_smem(a2, ctx->sms, ctx->stream));
+        }
+        return GERBIL_OK;
+      }));
       pre.out_n = hc.out_n;
       pre.sum_counts = hc.sum_counts;
       pre.distinct = hc.distinct;
@@ -625,8 +674,9 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   if (!rest.empty() && ref_tier1(ctx, k) && ctx->cfg.count_mode != 1) {
     std::vector<RestBin> keep;
     std::vector<std::vector<RestBin>> by_p(7);  // P = 2, 4, ..., 128
+    const uint32_t mf_full = ref_max_fill(cap_full);  // the passes use full-size tables
     for (const RestBin& rb : rest) {
-      const uint64_t want = (3 * rb.win + 2 * (uint64_t)max_fill - 1) / (2 * (uint64_t)std::max<uint32_t>(max_fill, 1));
+      const uint64_t want = (3 * rb.win + 2 * (uint64_t)mf_full - 1) / (2 * (uint64_t)std::max<uint32_t>(mf_full, 1));
       int e = 1;
       while (e < 7 && (1ull << e) < want) ++e;
       if ((1ull << e) >= want && rb.win < (1ull << 24)) by_p[e - 1].push_back(rb);
@@ -644,9 +694,6 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
         r2[2 * i + 1] = L[i].d1 | (L[i].win << kRangeWinShift);
         wsum += L[i].win;
       }
-      const uint64_t out2 = pre.out_n + wsum;
-      CK(ensure_keep(ctx->out_keys, out2 * W * 8, pre.out_n * W * 8, ctx->stream));
-      CK(ensure_keep(ctx->out_counts, out2 * 4, pre.out_n * 4, ctx->stream));
       CK(ctx->smem_range.ensure(L.size() * 16));
       CK(ctx->smem_failed.ensure(L.size() * 16 + 16));
       CK(cudaMemcpyAsync(ctx->smem_range.p, r2, L.size() * 16, cudaMemcpyHostToDevice, ctx->stream));
@@ -654,28 +701,27 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       SmemCountArgs a3 = a;
       a3.range = ctx->smem_range.as<unsigned long long>();
       a3.n_list = (uint32_t)L.size();
-      a3.out_keys = ctx->out_keys.as<uint64_t>();
-      a3.out_counts = ctx->out_counts.as<uint32_t>();
-      a3.out_cap = out2;
       a3.failed = ctx->smem_failed.as<unsigned long long>();
       a3.parts = P;
-      for (uint32_t q = 0; q < P; ++q) {
-        a3.part = q;
-        if (streaming) {
-          CK(cudaStreamSynchronize(ctx->pcie_stream));
-          rec_done = 0;
-          CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
-          CK(ctx->rec_stage2.ensure(std::max<uint64_t>(wsum, 1) * rec_max + 64));
-          CKS(stream_slices(a3, (uint32_t)L.size(), 1));
-        } else {
-          Timer tm(ctx, K_SMEM);
-          CK(launch_count_smem(a3, ctx->sms, ctx->stream));
+      a3.cap = cap_full;
+      a3.max_fill = mf_full;
+      a3.warps = -1;
+      CKS(run_pass(pre, wsum, [&](uint64_t* ok, uint32_t* oc, uint64_t cap_n) -> gerbil_status {
+        a3.out_keys = ok;
+        a3.out_counts = oc;
+        a3.out_cap = cap_n;
+        for (uint32_t q = 0; q < P; ++q) {
+          a3.part = q;
+          if (streaming) {
+            CKS(stream_slices(a3, (uint32_t)L.size(), 1));
+          } else {
+            Timer tm(ctx, K_SMEM);
+            CK(launch_count_smem(a3, ctx->sms, ctx->stream));
+          }
         }
-      }
-      CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
-      CK(cudaStreamSynchronize(ctx->stream));
+        return GERBIL_OK;
+      }));
       if (hc.read_work) return fail(ctx, GERBIL_E_INTERNAL, "hash-class pass overflowed a reference table");
-      if (hc.out_n > out2) return fail(ctx, GERBIL_E_INTERNAL, "hash-class pass result bound violated");
       pre.out_n = hc.out_n;
       pre.sum_counts = hc.sum_counts;
       pre.distinct = hc.distinct;

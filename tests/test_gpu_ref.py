@@ -61,7 +61,8 @@ def test_ref_abandoned_bin_goes_to_wave_tables(G):
     ref = oracle.count(text, 150, 1)
     keys, counts, st = _run(G, text, 150, 11, 1, n_bins=1, count_mode=G.COUNT_SMEM)
     compare(keys, counts, 150, ref)
-    assert st["smem_failed"] == 1 and st["count_sum"] == ref.windows
+    # abandoned by the half tables of tier 1 and again by the full-size table of tier 2
+    assert st["smem_failed"] >= 1 and st["count_sum"] == ref.windows
 
 
 def test_ref_repeats_and_low_complexity(G):
@@ -89,3 +90,18 @@ def test_ref_non_canonical(G):
     keys, counts, st = _run(G, text, 130, 11, 1, n_bins=16, canonical=False)
     compare(keys, counts, 130, ref)
     assert st["count_sum"] == ref.windows
+
+
+@pytest.mark.parametrize("k,read_len,n_reads", [(100, 150, 3000), (97, 2000, 200), (200, 3000, 150), (300, 2500, 120)])
+def test_ref_zero_fingerprints(G, monkeypatch, k, read_len, n_reads):
+    # GERBIL_REF_DBG=16 zeroes the fingerprints: every occupied slot a probe meets is compared
+    # k-mer by k-mer, so the verification (inline and the rolling path's deferred queue) and the
+    # re-probe after a mismatch run on nearly every window; counts must stay exact
+    monkeypatch.setenv("GERBIL_REF_DBG", "16")
+    w = synth.Workload(seed=900 + k, genome_len=40_000, read_len=read_len, n_reads=n_reads, err=0.01)
+    text = synth.fastx(w, synth.FASTA)
+    for min_count in (1, 2):
+        ref = oracle.count(text, k, min_count)
+        keys, counts, st = _run(G, text, k, 11, min_count, n_bins=1 << 16)
+        compare(keys, counts, k, ref)
+        assert st["count_sum"] == ref.windows and st["smem_windows"] == ref.windows
