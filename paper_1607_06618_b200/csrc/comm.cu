@@ -155,16 +155,23 @@ struct LoopGroup {
   std::vector<const void*> send;
   std::vector<const size_t*> soff, sbytes;
   explicit LoopGroup(int w) : world(w), send(w), soff(w), sbytes(w) {}
-  void barrier() {
+  // false when the peers did not all arrive within GERBIL_LOOPBACK_TIMEOUT_S (default 120 s):
+  // a virtual rank that failed and left the collective must not hang the others
+  bool barrier() {
+    static const long tmo = [] {
+      const char* e = getenv("GERBIL_LOOPBACK_TIMEOUT_S");
+      const long v = e ? atol(e) : 0;
+      return v > 0 ? v : 120L;
+    }();
     std::unique_lock<std::mutex> lk(mu);
     unsigned g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return true;
     }
+    return cv.wait_for(lk, std::chrono::seconds(tmo), [&] { return gen != g; });
   }
 };
 
@@ -176,13 +183,19 @@ class LoopComm : public Comm {
   std::shared_ptr<LoopGroup> g;
   bool allgather(const void* s, void* r, size_t bytes, cudaStream_t st) override {
     g->send[rank] = s;
-    g->barrier();
+    if (!g->barrier()) {
+      err = "loopback allgather: timed out waiting for the peers";
+      return false;
+    }
     bool ok = true;
     for (int p = 0; p < world; ++p)
       ok &= cudaMemcpyAsync((char*)r + p * bytes, g->send[p], bytes, cudaMemcpyDeviceToDevice, st) ==
             cudaSuccess;
     ok &= cudaStreamSynchronize(st) == cudaSuccess;
-    g->barrier();
+    if (!g->barrier()) {
+      err = "loopback allgather: timed out waiting for the peers";
+      return false;
+    }
     if (!ok) err = "loopback allgather copy failed";
     return ok;
   }
@@ -197,7 +210,10 @@ class LoopComm : public Comm {
       g->send[rank] = x[b].send;
       g->soff[rank] = x[b].send_off;
       g->sbytes[rank] = x[b].send_bytes;
-      g->barrier();
+      if (!g->barrier()) {
+        err = "loopback alltoallv: timed out waiting for the peers";
+        return false;
+      }
       for (int p = 0; p < world; ++p) {
         const size_t m = g->sbytes[p][rank];
         if (m != x[b].recv_bytes[p]) ok = false;
@@ -206,7 +222,10 @@ class LoopComm : public Comm {
                                 cudaMemcpyDeviceToDevice, st) == cudaSuccess;
       }
       ok &= cudaStreamSynchronize(st) == cudaSuccess;
-      g->barrier();
+      if (!g->barrier()) {
+        err = "loopback alltoallv: timed out waiting for the peers";
+        return false;
+      }
     }
     if (!ok) err = "loopback alltoallv size mismatch or copy failure";
     return ok;

@@ -405,6 +405,7 @@ gerbil_status gerbil_spill_finish(gerbil_ctx* ctx, uint32_t min_count, uint8_t* 
   if (const char* e = getenv("GERBIL_SPILL_GROUP_BYTES"))
     if (*e) budget = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
   SpillAcc acc;
+  CK(ctx->counters.ensure(sizeof(Counters)));  // a rank that spilled nothing ran no step (b)
   gerbil_status st = GERBIL_OK;
   if (ctx->world > 1) st = spill_finish_ranks(ctx, min_count, budget, acc);
   for (uint32_t b = 0; b < B && ctx->world == 1; ++b) acc.max_bin = std::max<uint64_t>(acc.max_bin, sp.win[b]);

@@ -83,6 +83,7 @@ gerbil_status count_waves_l2(gerbil_ctx* ctx, const uint64_t* stream_codes, cons
     CK(ctx->wave_distinct.ensure(2 * nw * 8));
     CK(cudaMemsetAsync(ctx->table.p, 0, lanes * lane_bytes, ctx->stream));
     CK(cudaMemsetAsync(ctx->wave_distinct.p, 0, 2 * nw * 8, ctx->stream));
+    CK(ctx->counters.ensure(sizeof(Counters)));  // a rank that ran no step (b) (empty spill) has none yet
     Counters* dc = ctx->counters.as<Counters>();
     CK(cudaMemsetAsync(&dc->ovf_n, 0, sizeof(Counters) - offsetof(Counters, ovf_n), ctx->stream));
     if (pre.out_n || pre.sum_counts || pre.distinct) {
@@ -545,14 +546,15 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   // input the bound is far larger than what is kept); if the kept results do not fit, the pass is
   // rerun once with the exact size after the counters are restored to `base`.
   auto run_pass = [&](const Preset& base, uint64_t bound, auto&& issue) -> gerbil_status {
-    // entries the buffers could hold: their present size plus 85 % of the free device memory
+    // entries the buffers can hold without failing: their present capacity, or a new pair of buffers
+    // in 80 % of the free device memory (growing allocates the new buffer before the old is freed)
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
       cudaGetLastError();
       fr = 0;
     }
-    const uint64_t room = (uint64_t)((fr * 0.85 + (double)ctx->out_keys.bytes + (double)ctx->out_counts.bytes) /
-                                     (W * 8.0 + 4.0));
+    const uint64_t have = std::min<uint64_t>(ctx->out_keys.bytes / (W * 8ull), ctx->out_counts.bytes / 4ull);
+    const uint64_t room = std::max<uint64_t>(have, (uint64_t)(fr * 0.8 / (W * 8.0 + 4.0)));
     const uint64_t grow = std::max<uint64_t>(room > base.out_n ? room - base.out_n : 0,
                                              std::max<uint64_t>(result_budget_entries(ctx, W, 5), 1));
     uint64_t cap_n = base.out_n + std::min<uint64_t>(std::max<uint64_t>(bound, 1), grow);
