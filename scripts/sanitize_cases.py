@@ -23,6 +23,9 @@ CASES = {
     "smem_alla": (lambda: ALLA, 40, 15, 1, dict(n_bins=1 << 16)),
     "ref_k150": (lambda: synth.fastx(LONG, synth.FASTA), 150, 15, 1, dict(n_bins=1 << 16)),
     "ref_alla": (lambda: ALLA, 150, 11, 1, dict(n_bins=4)),
+    # GERBIL_REF_DBG=16 (zero fingerprints): every occupied slot met is verified, the deferred
+    # queue and the re-probe after a mismatch run constantly
+    "ref_k200_zfp": (lambda: synth.fastx(LONG, synth.FASTA), 200, 15, 2, dict(n_bins=1 << 16)),
     "l2_k28": (lambda: synth.fastx(C0, synth.FASTQ), 28, 7, 1, dict(n_bins=1, count_mode=gerbil.COUNT_L2)),
     "l2_k200": (lambda: synth.fastx(LONG, synth.FASTA), 200, 11, 2, dict(n_bins=16, count_mode=gerbil.COUNT_L2)),
     "l2_overflow": (lambda: synth.fastx(C0, synth.FASTQ), 33, 9, 1,
@@ -38,6 +41,10 @@ CASES = {
 
 def run(name):
     text_fn, k, m, mc, kw = CASES[name]
+    if name.endswith("_zfp"):
+        os.environ["GERBIL_REF_DBG"] = "16"
+    else:
+        os.environ.pop("GERBIL_REF_DBG", None)
     text = text_fn()
     ref = oracle.count(text, k, mc)
     with gerbil.Gerbil(**kw) as g:
