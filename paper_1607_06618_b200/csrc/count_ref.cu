@@ -40,6 +40,12 @@ constexpr uint32_t kFull = 0xffffffffu;
 // Threads per SM: one CTA of 512 (one bin in flight per SM, the whole shared memory its table)
 // or two CTAs of 256 (two bins in flight, half tables): the kernel's template parameter NT.
 constexpr int kRefSmThreads = 512;
+#ifndef GERBIL_REF_T1_NT
+#define GERBIL_REF_T1_NT 256  // threads of each of the two tier-1 CTAs per SM
+#endif
+constexpr int kRefT1Threads = GERBIL_REF_T1_NT;
+template <int NT>
+constexpr int ref_ctas_per_sm() { return NT == kRefSmThreads ? 1 : 2; }
 constexpr uint32_t kLongSm = 32;                 // mean windows per super-mer from which a bin is cut in pieces
 constexpr uint64_t kOcc = 1ull << 63;
 constexpr int kFpShift = 40;
@@ -167,7 +173,7 @@ __device__ __noinline__ bool rc_is_less(const uint64_t* codes, uint64_t q, uint3
 }
 
 template <int W, int NT>
-__global__ void __launch_bounds__(NT, kRefSmThreads / NT) count_ref_kernel(SmemCountArgs a) {
+__global__ void __launch_bounds__(NT, ref_ctas_per_sm<NT>()) count_ref_kernel(SmemCountArgs a) {
   constexpr int kRefThreads = NT;  // warps per bin = kRefThreads / 32
   constexpr int kRefWarps = kRefThreads / 32;
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -641,7 +647,7 @@ cudaError_t launch_ref_nt(const SmemCountArgs& a, int sms, cudaStream_t st) {
   if (const char* ev = getenv("GERBIL_REF_DBG")) b.dbg = (uint32_t)atoi(ev);
   cudaError_t e = cudaFuncSetAttribute(count_ref_kernel<W, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
-  uint64_t grid = (uint64_t)sms * (kRefSmThreads / NT);
+  uint64_t grid = (uint64_t)sms * ref_ctas_per_sm<NT>();
   if (grid > a.n_list) grid = a.n_list;
   if (grid == 0) return cudaSuccess;
   count_ref_kernel<W, NT><<<(unsigned)grid, NT, dyn, st>>>(b);
@@ -651,7 +657,7 @@ cudaError_t launch_ref_nt(const SmemCountArgs& a, int sms, cudaStream_t st) {
 // a.warps = -2: two 256-thread CTAs per SM (a.cap = ref_table_slots(.., 2)); else one of 512
 template <int W>
 cudaError_t launch_ref_w(const SmemCountArgs& a, int sms, cudaStream_t st) {
-  return a.warps == -2 ? launch_ref_nt<W, kRefSmThreads / 2>(a, sms, st) : launch_ref_nt<W, kRefSmThreads>(a, sms, st);
+  return a.warps == -2 ? launch_ref_nt<W, kRefT1Threads>(a, sms, st) : launch_ref_nt<W, kRefSmThreads>(a, sms, st);
 }
 
 }  // namespace
@@ -662,7 +668,7 @@ uint32_t ref_table_slots(size_t smem_per_block, int ctas_per_sm) {
   // CTAs sharing an SM each get their share of its shared memory (the opt-in per-block maximum
   // + the 1 KB the runtime reserves per block), minus that reserve and the static arrays
   const int ctas = ctas_per_sm == 2 ? 2 : 1;
-  const size_t nt = kRefSmThreads / ctas;
+  const size_t nt = ctas == 2 ? (size_t)kRefT1Threads : (size_t)kRefSmThreads;
   const size_t share = (smem_per_block + 1024) / ctas;
   const size_t stat = nt * 13 + 256 + (GERBIL_REF_DEFER ? nt / 32 * 64 * 8 : 0);  // static shared arrays
   const size_t avail = share > 1024 + stat ? share - 1024 - stat : 0;

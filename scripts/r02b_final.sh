@@ -18,18 +18,20 @@ if [ "${LAUNCH:-1}" = "1" ]; then
 run launches "timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1"
 fi
 if [ "${NCU:-1}" = "1" ]; then
-# count_ref_kernel: every launch of 4 calls (tier 1, tier 2, hash-class passes)
-nref=$(python -c "import json;print(json.load(open('gpurun_out/r02_bench_C4.json'))['roofline']['launches_per_step'])" 2>/dev/null || echo 3)
-for spec in ${PROF:-c1_supermer:C1:supermer_kernel:3:1 c1_smem:C1:count_smem_kernel:0:8 c1_part:C1:partition64:0:8 c1_regroup:C1:regroup_counted:3:1 c1_ghist:C1:group_hist:3:1 c4_ref:C4:count_ref_kernel:0:$((4 * nref)) c4_supermer:C4:supermer_kernel:3:1}; do
-  IFS=: read name cfg rx skip cnt <<< "$spec"
-  run ncu_$name "timeout 1800 ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c $cnt -o gpurun_out/prof_$name -f python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_$name.log 2>&1"
+# count_ref_kernel: the tier-1 launch of the first call (~90 % of the tier time; a --set full replay
+# of all 16 launches of a call saves and restores tens of GB per pass: > 30 min)
+nref=$(python -c "import json;print(json.load(open('gpurun_out/r02_bench_C4.json'))['roofline']['launches_per_step'])" 2>/dev/null || echo 16)
+for spec in ${PROF:-c1_supermer:C1:supermer_kernel:3:1:3 c1_smem:C1:count_smem_kernel:0:8:3 c1_part:C1:partition64:0:8:3 c1_regroup:C1:regroup_counted:3:1:3 c1_ghist:C1:group_hist:3:1:3 c4_ref:C4:count_ref_kernel:0:1:0 c4_supermer:C4:supermer_kernel:3:1:3}; do
+  IFS=: read name cfg rx skip cnt wu <<< "$spec"
+  run ncu_$name "timeout 1800 ncu --set full --clock-control none --import-source on -k regex:$rx -s $skip -c $cnt -o gpurun_out/prof_$name -f python bench.py --config $cfg --steps 1 --warmup $wu --no-e2e --no-cpu-baseline > gpurun_out/ncu_$name.log 2>&1"
   ncu -i gpurun_out/prof_$name.ncu-rep --page raw --csv > gpurun_out/raw_$name.csv 2>/dev/null
   ncu -i gpurun_out/prof_$name.ncu-rep > gpurun_out/details_$name.txt 2>/dev/null
   python scripts/ncu_srcprof.py gpurun_out/prof_$name.ncu-rep 60 > gpurun_out/src_$name.txt 2>/dev/null
   rm -f gpurun_out/prof_$name.ncu-rep  # the merge-back limit is 64 MiB: keep the exports only
 done
 fi
-if [ "${SAN:-1}" = "1" ]; then
+# compute-sanitizer is closed on this pool (runs under it left GPUs needing a reset): off by default
+if [ "${SAN:-0}" = "1" ]; then
 for tool in memcheck racecheck synccheck; do
   extra=""
   [ "$tool" = "racecheck" ] && extra="--racecheck-report analysis"

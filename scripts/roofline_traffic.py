@@ -6,8 +6,8 @@ from the ncu --set full raw exports of scripts/r02_final.sh (gpurun_out/raw_<nam
 Per capture: DRAM bytes read + written (dram__bytes_read.sum + dram__bytes_write.sum), warp
 instructions (smsp__inst_executed.sum), duration, IPC, issue-slot use, achieved occupancy, L2 hit
 rate, L2 atomic / reduction sectors. For count_smem_kernel (8 launches = the two tiers of 4 calls)
-the timed step is the last two launches; count_ref_kernel captures hold all launches of 4 calls (tier 1,
-tier 2, hash-class passes), the timed step is the last quarter.
+the timed step is the last two launches; count_ref_kernel captures hold every launch of one call (tier 1,
+tier 2, hash-class passes).
 """
 import csv
 import json
@@ -64,7 +64,7 @@ SPECS = {  # capture name: (config, kernel label, launches per timed step)
     "c1_part": ("C1", "partition64_kernel", 2),
     "c1_regroup": ("C1", "regroup_counted_kernel", 1),
     "c1_ghist": ("C1", "group_hist_kernel", 1),
-    "c4_ref": ("C4", "count_ref_kernel", None),  # every reference-table launch of 4 calls: the last quarter
+    "c4_ref": ("C4", "count_ref_kernel", 1),  # the tier-1 launch (~90 % of the reference-table time)
     "c4_supermer": ("C4", "supermer_kernel", 1),
 }
 
@@ -80,7 +80,7 @@ def main():
         if not launches:
             continue
         if per_step is None:
-            per_step = max(1, len(launches) // 4)
+            per_step = len(launches)
         step = launches[-per_step:]
         tot = lambda k: sum(x.get(k, 0.0) for x in step)  # noqa: E731
         dram = tot("dram_read") + tot("dram_write")
