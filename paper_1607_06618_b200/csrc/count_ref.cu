@@ -37,11 +37,13 @@ namespace gerbil {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-// Threads per SM: one CTA of 512 (one bin in flight per SM, the whole shared memory its table)
-// or two CTAs of 256 (two bins in flight, half tables): the kernel's template parameter NT.
+// Threads per CTA (the kernel's template parameter NT): one CTA of 512 per SM (one bin in flight,
+// the whole shared memory its table), or two CTAs per SM (two bins in flight, half tables) of
+// GERBIL_REF_T1_NT threads each — 384 (80 registers, a small L1-resident spill) beat 256 at C4
+// by 20 ms: the kernel is latency-bound, more warps hide more of it.
 constexpr int kRefSmThreads = 512;
 #ifndef GERBIL_REF_T1_NT
-#define GERBIL_REF_T1_NT 256  // threads of each of the two tier-1 CTAs per SM
+#define GERBIL_REF_T1_NT 384
 #endif
 constexpr int kRefT1Threads = GERBIL_REF_T1_NT;
 template <int NT>

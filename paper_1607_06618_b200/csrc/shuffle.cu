@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(kFineThreads) regroup_fine_packed_kernel(const
 constexpr int kGroupShift = 10;   // fine bins per group = 1024
 constexpr int kDigits = 64;       // buckets per partition pass
 constexpr int kPartThreads = 256;
-constexpr int kPartPer = 16;
+#ifndef GERBIL_PART_PER
+#define GERBIL_PART_PER 8  // elements per thread and chunk (registers: ~8 per element; 8 at 4 CTAs/SM beat 16 at 2)
+#endif
+constexpr int kPartPer = GERBIL_PART_PER;
 constexpr int kPartChunk = kPartThreads * kPartPer;
 
 __global__ void __launch_bounds__(256) group_hist_kernel(const uint32_t* __restrict__ bin, uint64_t n, uint32_t G,
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(1024) part_setup_kernel(const unsigned long lo
 // One partition pass (A: n_seg == 1 over [0, n); B: n_seg segments from seg[], chunks
 // numbered per chunk_first[]). digit = (bin >> shift) & 63; cursors cur[seg * 64 + digit].
 #ifndef GERBIL_PART_MINB
-#define GERBIL_PART_MINB 2
+#define GERBIL_PART_MINB 4
 #endif
 template <bool PACK_OUT>
 __global__ void __launch_bounds__(kPartThreads, GERBIL_PART_MINB) partition64_kernel(

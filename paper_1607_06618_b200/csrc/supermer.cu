@@ -116,8 +116,8 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 // blocks + the prefix of one later block (shared memory); the w-1 keys past the tile's 1024
 // positions are computed one per lane by warps 0-1 (prefix minima by 8-lane shuffle scans).
 #ifndef GERBIL_SM_MINB_A8
-#define GERBIL_SM_MINB_A8 12  // A8: 40 registers, 12 CTAs (48 warps) per SM — more warps hide the tile barriers
-#endif                        // better than the few bytes of L1-resident spill cost (C1: 22.4 -> 20.7 ms)
+#define GERBIL_SM_MINB_A8 16  // A8: 32 registers (no spill), 16 CTAs (64 warps) per SM — more warps hide the tile barriers
+#endif                        // (C1: 8 CTAs 22.4 ms, 12: 20.7 ms, 16: 19.8 ms)
 template <uint32_t ORD, int KMAX, uint32_t MT, bool A8 = false>  // MT: m fixed at compile time (0 = runtime a.m)
 __global__ void __launch_bounds__(kThreads, A8 ? GERBIL_SM_MINB_A8 : GERBIL_SM_MINB)
 supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t tile_begin, uint64_t tile_end,

@@ -546,18 +546,11 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   // input the bound is far larger than what is kept); if the kept results do not fit, the pass is
   // rerun once with the exact size after the counters are restored to `base`.
   auto run_pass = [&](const Preset& base, uint64_t bound, auto&& issue) -> gerbil_status {
-    // entries the buffers can hold without failing: their present capacity, or a new pair of buffers
-    // in 80 % of the free device memory (growing allocates the new buffer before the old is freed)
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-      cudaGetLastError();
-      fr = 0;
-    }
+    // the buffers' present capacity (no reallocation in steady state: a grown buffer is kept), or
+    // room for a budget's worth of results after base; a first call that outgrows it reruns once
     const uint64_t have = std::min<uint64_t>(ctx->out_keys.bytes / (W * 8ull), ctx->out_counts.bytes / 4ull);
-    const uint64_t room = std::max<uint64_t>(have, (uint64_t)(fr * 0.8 / (W * 8.0 + 4.0)));
-    const uint64_t grow = std::max<uint64_t>(room > base.out_n ? room - base.out_n : 0,
-                                             std::max<uint64_t>(result_budget_entries(ctx, W, 5), 1));
-    uint64_t cap_n = base.out_n + std::min<uint64_t>(std::max<uint64_t>(bound, 1), grow);
+    const uint64_t budget = std::max<uint64_t>(result_budget_entries(ctx, W, 5), 1);
+    uint64_t cap_n = std::max<uint64_t>(have, base.out_n + std::min<uint64_t>(std::max<uint64_t>(bound, 1), budget));
     const uint64_t host_start = host_off;
     for (int attempt = 0;; ++attempt) {
       CK(ensure_keep(ctx->out_keys, cap_n * W * 8, base.out_n * W * 8, ctx->stream));
@@ -566,7 +559,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
         CK(cudaStreamSynchronize(ctx->pcie_stream));
         rec_done = 0;
         CK(cudaMemsetAsync(ctx->rec_meta.p, 0, 2 * 8, ctx->stream));
-        CK(ctx->rec_stage2.ensure((cap_n - base.out_n) * rec_max + 64));
+        CK(ctx->rec_stage2.ensure(std::min<uint64_t>(cap_n - base.out_n, std::max<uint64_t>(bound, 1)) * rec_max + 64));
       }
       CKS(issue(ctx->out_keys.as<uint64_t>(), ctx->out_counts.as<uint32_t>(), cap_n));
       CK(d2h_small(ctx, ctx->h_counters, dc, sizeof(Counters)));
