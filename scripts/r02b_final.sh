@@ -7,6 +7,9 @@ mkdir -p gpurun_out
 python build_native.py > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
 { nproc; lscpu | grep -E "Model name|^CPU\(s\)"; nvidia-smi --query-gpu=name,clocks.max.sm --format=csv; } > gpurun_out/host.txt 2>&1
 run() { echo "== $1" >> gpurun_out/summary.txt; s=$(date +%s); bash -c "$2"; echo "   rc=$? $(( $(date +%s) - s )) s" >> gpurun_out/summary.txt; }
+if [ "${TESTS:-1}" = "1" ]; then
+run gpu_tests "timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 > gpurun_out/r02_gpu_tests.txt 2>&1"
+fi
 if [ "${BENCH:-1}" = "1" ]; then
 run bench_c1 "timeout 1200 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err"
 run bench_ref "timeout 900 python bench.py --impl reference > gpurun_out/r02_bench_reference.json 2> gpurun_out/r02_bench_reference.err"
