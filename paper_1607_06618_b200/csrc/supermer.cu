@@ -111,10 +111,10 @@ __global__ void rs_bits_kernel(const uint64_t* __restrict__ read_start, uint64_t
 #ifndef GERBIL_SM_MINB
 #define GERBIL_SM_MINB 8  // CTAs per SM the register budget is sized for (8: 64 regs; occupancy beats the small L1-resident spill)
 #endif
-// A8 (w = k-m+1 <= 129, the KMAX = 200 geometry): key blocks of 8 aligned with the thread's 8
+// A8 (w = k-m+1 <= 193, the KMAX = 200 geometry): key blocks of 8 aligned with the thread's 8
 // windows, so a window's minimum is the suffix of the thread's OWN block (registers) + whole
 // blocks + the prefix of one later block (shared memory); the keys past the tile's 1024
-// positions (up to 128) are computed one per thread (prefix minima by 8-lane shuffle scans).
+// positions (up to 192) are computed one or two per thread (prefix minima by 8-lane shuffle scans).
 #ifndef GERBIL_SM_MINB_A8
 #define GERBIL_SM_MINB_A8 16  // A8: 32 registers (no spill), 16 CTAs (64 warps) per SM — more warps hide the tile barriers
 #endif                        // (C1: 8 CTAs 22.4 ms, 12: 20.7 ms, 16: 19.8 ms)
@@ -131,7 +131,7 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
   __shared__ uint32_t s_key[kKeyLen];    // c_j
   __shared__ uint32_t s_pre[kKeyLen];    // min over c[8b .. j] (j in block b)
   __shared__ uint32_t s_suf[kKeyLen];    // min over c[j .. 8b+7]
-  __shared__ uint32_t s_blk[kKeyBlocks + 16]; // min over block b (A8: 16 more blocks past the tile)
+  __shared__ uint32_t s_blk[kKeyBlocks + 24]; // min over block b (A8: 24 more blocks past the tile)
   __shared__ uint32_t s_brk[kSTile / 32 + 1];
   __shared__ uint32_t s_last[kThreads];  // μ of window 8t+7, or ~0 if invalid
   __shared__ uint16_t s_sp[kSTile];      // the tile's super-mer start positions
@@ -222,10 +222,11 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
         }
         s_blk[tid] = pre;
       }
-      // the keys past the tile (positions 1024 .. 1024+w-2 <= 1151): one per thread of warps 0-1
-      // (w <= 65) or of all four warps (warp-uniform)
-      if (tid < 64 || w > 65) {
-        const uint32_t j = kSTile + tid, wi = j >> 5, sh = (j & 31) * 2;
+      // the keys past the tile (positions 1024 .. 1024+w-2 <= 1215): position 1024+i by thread i,
+      // 1152+i by thread i of warps 0-1; only the warps whose positions some window reaches
+      // (warp-uniform conditions)
+      auto extra_key = [&](uint32_t j) {
+        const uint32_t wi = j >> 5, sh = (j & 31) * 2;
         const uint64_t v = sh ? ((s_codes[wi] << sh) | (s_codes[wi + 1] >> (64 - sh))) : s_codes[wi];
         const uint32_t f = (uint32_t)(v >> (64 - 2 * m)) & mmask;
         const uint32_t rc = (uint32_t)(rev_pairs(~v) & mmask);
@@ -238,7 +239,9 @@ supermer_kernel(SupermerArgs a, const uint64_t* __restrict__ rs_bits, uint64_t t
         }
         s_pre[j] = x;
         if ((lane & 7) == 7) s_blk[j >> 3] = x;
-      }
+      };
+      if (tid < 64 || w > 65) extra_key(kSTile + tid);
+      if (tid < 64 && w > 129) extra_key(kSTile + 128 + tid);
       __syncthreads();
       // 3'. minimizers of windows 8t+i = min(suffix of c from i, whole blocks, prefix at the end)
       uint32_t suf[kPer];
@@ -499,7 +502,7 @@ cudaError_t supermer_run_tiles(const SupermerArgs& a, const uint64_t* rs_bits, u
     const char* e = getenv("GERBIL_SM_A8");
     return !(e && atoi(e) == 0);
   }();
-  if (a.ordering == kOrdKMC2 && !wide && a.k - a.m + 1 <= 129 && a8_on) {
+  if (a.ordering == kOrdKMC2 && !wide && a.k - a.m + 1 <= 193 && a8_on) {
     if (a.m == 15) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 15, true>);
     if (a.m == 11) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 11, true>);
     if (a.m == 7) return go(supermer_kernel<kOrdKMC2, kMaxKSmall, 7, true>);
