@@ -591,11 +591,21 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
   // the full-size reference table: tier 2 after half tables in tier 1 (W >= 4, two CTAs per SM),
   // tier 2 for mostly distinct short keys, and the hash-class passes below
   const uint32_t cap_full = ref_table_slots((size_t)ctx->smem_optin - 1024, 1);
-  const bool ref2 = tier2_ref || (tier1_ref && a.warps == -2);
-  const uint32_t cap2 = ref2 ? cap_full
-                        : tier1_ref ? 0u
-                                    : (w1 > 4 ? smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n) : 0u);
-  if (!rest.empty() && cap2 > cap) {
+  // the tier-2 passes, in order: (table slots, warps per CTA; -1 / -2 = reference tables with
+  // one / two CTAs per SM). Mostly distinct short keys first try two half-size reference tables
+  // per SM (bins of the C2/C3 shards hold ~10^3 windows: half tables take nearly all of them,
+  // and two bins in flight per SM hide the per-bin barriers), then one full-size table per SM.
+  std::vector<std::pair<uint32_t, int>> tiers;
+  if (tier1_ref && a.warps == -2) {
+    tiers.push_back({cap_full, -1});
+  } else if (tier2_ref) {
+    if (ref_tier1_ctas() == 2) tiers.push_back({ref_table_slots((size_t)ctx->smem_optin - 1024, 2), -2});
+    tiers.push_back({cap_full, -1});
+  } else if (!tier1_ref && w1 > 4) {
+    tiers.push_back({smem_table_slots(k, (size_t)ctx->smem_optin - 1024, w2n), w2n});
+  }
+  auto tier_pass = [&](uint32_t cap2, int warps2) -> gerbil_status {
+    const bool ref2 = warps2 < 0;
     const uint32_t mf2 = ref2 ? ref_max_fill(cap2) : cap2 - std::max<uint32_t>(64u, cap2 / 4);
     const uint64_t thr2 = smem_window_threshold(ctx, mf2);
     std::vector<RestBin> keep;
@@ -623,7 +633,7 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       a2.n_list = (uint32_t)n2;
       a2.cap = cap2;
       a2.max_fill = mf2;
-      a2.warps = ref2 ? -1 : w2n;  // -1: the CTA-wide reference tables, one per SM
+      a2.warps = warps2;  // -1 / -2: the CTA-wide reference tables, one / two per SM
       a2.failed = ctx->smem_failed.as<unsigned long long>();
       CKS(run_pass(pre, ob2, [&](uint64_t* ok, uint32_t* oc, uint64_t cap_n) -> gerbil_status {
         a2.out_keys = ok;
@@ -657,9 +667,12 @@ gerbil_status count_waves_ranges(gerbil_ctx* ctx, const uint64_t* stream_codes, 
       ctx->stats.smem_failed += nf2;
       smem_windows += w2 - std::min(w2, fw2);
       rest.swap(keep);
-      trace("smem tier 2 done (synced)");
+      trace("smem tier 2 pass done (synced)");
     }
-  }
+    return GERBIL_OK;
+  };
+  for (const auto& t : tiers)
+    if (!rest.empty() && (t.second < 0 || t.first > cap)) CKS(tier_pass(t.first, t.second));
   // Long keys (reference tables in tier 1): a bin too large for one CTA table is counted in P
   // passes over its super-mers, pass p keeping the k-mers whose hash class is p (distinct k-mers
   // spread evenly over the classes: P = 1.5 x windows / max_fill (distinct <= windows) leaves each
