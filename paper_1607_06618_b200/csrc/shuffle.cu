@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(kPartThreads, GERBIL_PART_MINB) partition64_ke
 
 // Pass C: one CTA per group. Fine-bin counts and windows, the bins' offsets/windows out,
 // then the scatter into bin order (descriptor bits 54.. cleared).
+#ifndef GERBIL_REGROUP_STAGE
+#define GERBIL_REGROUP_STAGE 1
+#endif
 constexpr int kFineT = 512;
 constexpr int kFineU = 8;
 template <bool WIDE>  // WIDE: a fine bin may hold >= 2^32 windows (u64 shared counters, CAS loops)
@@ -425,6 +428,65 @@ __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t*
   }
   if (b0 + kFan >= n_bins && tid == 0) off[n_bins] = i1;  // the last group closes the offsets
   __syncthreads();
+#if GERBIL_REGROUP_STAGE
+  // scatter in chunks of kFineT * kU descriptors staged in shared memory in fine-bin order:
+  // a bin's run of the chunk then leaves as consecutive 8-byte stores (round 2: one scattered
+  // store per descriptor left DRAM writes at ~2x the bytes)
+  constexpr int kU = WIDE ? kFineU / 2 : kFineU;  // WIDE: u64 window counters leave less room
+  __shared__ uint64_t s_stage[kFineT * kU];
+  __shared__ uint32_t s_lc[kFan];  // the chunk's count per fine bin, then its local offset
+  for (unsigned long long base = i0; base < i1; base += (unsigned long long)kFineT * kU) {
+    uint64_t d[kU];
+    uint32_t r[kU];
+    for (uint32_t t = tid; t < kFan; t += kFineT) s_lc[t] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const unsigned long long i = base + u * kFineT + tid;
+      d[u] = i < i1 ? __ldg(desc_in + i) : ~0ull;
+      if (d[u] != ~0ull) r[u] = atomicAdd(&s_lc[(uint32_t)(d[u] >> kDescPackShift)], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the chunk's 1024 counts (2 per thread), kept beside the counts
+    const uint32_t c0 = s_lc[2 * tid], c1 = s_lc[2 * tid + 1];
+    uint32_t in2 = c0 + c1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, in2, o);
+      if (lane >= (uint32_t)o) in2 += t;
+    }
+    if (lane == 31) s_w[warp] = in2;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = lane < kFineT / 32 ? s_w[lane] : 0u;
+      uint32_t y = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= (uint32_t)o) y += t;
+      }
+      if (lane < kFineT / 32) s_w[lane] = y - x;
+    }
+    __syncthreads();
+    const uint32_t e2 = s_w[warp] + in2 - c0 - c1;
+    s_lc[2 * tid] = e2;
+    s_lc[2 * tid + 1] = e2 + c0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (d[u] != ~0ull) s_stage[s_lc[(uint32_t)(d[u] >> kDescPackShift)] + r[u]] = d[u];
+    __syncthreads();
+    const uint32_t tot = i1 - base < (unsigned long long)(kFineT * kU) ? (uint32_t)(i1 - base) : kFineT * kU;
+    for (uint32_t x = tid; x < tot; x += kFineT) {
+      const uint64_t v = s_stage[x];
+      const uint32_t f = (uint32_t)(v >> kDescPackShift);
+      desc_out[i0 + s_cur[f] + (x - s_lc[f])] = v & kLow;
+    }
+    __syncthreads();
+    // the chunk's runs are placed: advance the bins' cursors (2 bins per thread)
+    s_cur[2 * tid] += c0;
+    s_cur[2 * tid + 1] += c1;
+    __syncthreads();
+  }
+#else
   for (unsigned long long base = i0; base < i1; base += (unsigned long long)kFineT * kFineU) {
     uint64_t d[kFineU];
     uint32_t p[kFineU];
@@ -440,6 +502,7 @@ __global__ void __launch_bounds__(kFineT) regroup_counted_kernel(const uint64_t*
     for (int u = 0; u < kFineU; ++u)
       if (d[u] != ~0ull) desc_out[i0 + p[u]] = d[u] & kLow;
   }
+#endif
 }
 
 // ---- multi-rank exchange of whole groups (a group = 1024 consecutive bins) ----------------
