@@ -111,16 +111,19 @@ typedef struct {
                                     x and rc(x) are different k-mers. 0 = canonical (default) */
   double dfp_pivot;        /* DFP ordering: pivot p in [0, 1] */
   uint32_t order_sample_stride; /* DFP ordering: sample every stride-th 1024-base tile; 0 = 16 */
-  int32_t count_mode;      /* step (d) table placement:
-                              0 = auto: a bin predicted (ρ̂ · windows) to fit one warp's
-                                  shared-memory table is counted there, the rest in
-                                  L2-resident wave tables; n_bins = 0 then picks enough bins
-                                  (up to 2^22) when m >= 11 makes bins that small and
-                                  k <= 96 (where it was measured to win);
+  int32_t count_mode;      /* step (d) table placement ("Kernel (d)"):
+                              0 = auto: a bin predicted (ρ̂ · windows) to fit an on-chip table
+                                  is counted there — one warp's shared-memory table of whole
+                                  keys (k <= 96), or a CTA's table of occurrence references
+                                  (k > 96; and the second tier of mostly distinct data); bins
+                                  too large go to hash-class passes (k > 96) or L2-resident
+                                  wave tables; n_bins = 0 then picks enough bins (up to 2^22)
+                                  when m >= 11 makes bins that small;
                               1 = L2 wave tables only;
-                              2 = try shared memory for every bin (test seam: bins that
-                                  overflow it are recounted in the wave tables).
-                              Results never depend on it. Streaming calls use 1. */
+                              2 = try the on-chip tables for every bin (test seam: bins that
+                                  overflow them are recounted in the wave tables).
+                              Results never depend on it; the streaming call uses the same
+                              placement. */
 } gerbil_config;
 
 /* Result encodings (App. C). */
@@ -167,10 +170,10 @@ typedef struct {
   double ms_reader;
   uint32_t launches_count, launches_compact, launches_total;
   /* step (d) in shared memory (count_mode != 1) */
-  uint64_t smem_bins;        /* bins counted in per-warp shared-memory tables */
-  uint64_t smem_failed;      /* of which abandoned (too many distinct k-mers) and recounted in L2 */
+  uint64_t smem_bins;        /* bins counted in on-chip (shared-memory) tables, all tiers */
+  uint64_t smem_failed;      /* of which abandoned (too many distinct k-mers) by a tier and passed on */
   uint64_t smem_windows;     /* windows of the bins that completed in shared memory */
-  uint32_t smem_slots;       /* table slots per warp */
+  uint32_t smem_slots;       /* first-tier table slots (per warp, or per CTA for reference tables) */
   uint32_t launches_smem;    /* shared-memory count launches (included in launches_count) */
   double ms_smem;            /* their device time (included in ms_count) */
 } gerbil_stats;

@@ -101,9 +101,22 @@ def main():
                      f"({dram / 1e9 / max(tot('ms') / 1e3, 1e-9):7.1f} GB/s)  {tot('inst') / 1e9:6.2f} G warp-inst  "
                      f"IPC {e['ipc']:.2f}  issue {100 * e['issue_slots_busy']:.0f}%  occ {100 * e['achieved_occupancy']:.0f}%"
                      f"  L2 hit {100 * e['l2_hit_rate']:.0f}%  atom {tot('atom') / 1e6:.1f} M  red {tot('red') / 1e6:.1f} M")
-    json.dump(table, open(os.path.join(os.path.dirname(prefix) or ".", "roofline_traffic.json"), "w"), indent=1)
-    with open(f"{prefix}_ncu_summary.txt", "w") as f:
-        f.write("# r02 ncu --set full captures (scripts/r02_final.sh), per timed step of bench.py\n")
+    # keep the entries (and summary lines) of kernels this capture set did not re-measure
+    jpath = os.path.join(os.path.dirname(prefix) or ".", "roofline_traffic.json")
+    spath = f"{prefix}_ncu_summary.txt"
+    got = {(e["config"], e["kernel"]) for e in table}
+    if os.path.exists(jpath):
+        for e in json.load(open(jpath)):
+            if (e.get("config"), e.get("kernel")) not in got:
+                table.append(e)
+    if os.path.exists(spath):
+        names = {ln.split()[0] for ln in lines}
+        for ln in open(spath).read().splitlines():
+            if ln and not ln.startswith("#") and ln.split()[0] not in names and ln.split()[0] in SPECS:
+                lines.append(ln)
+    json.dump(table, open(jpath, "w"), indent=1)
+    with open(spath, "w") as f:
+        f.write("# r02 ncu --set full captures (scripts/r02b_final.sh), per timed step of bench.py\n")
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
