@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace gerbil {
@@ -683,7 +684,11 @@ cudaError_t launch_group_shuffle(const GroupShuffleArgs& a, int sms, cudaStream_
   uint64_t* packed = n_seg > 1 ? a.desc_alt : a.tmp_desc;  // pass B output: never its own input
   partition64_kernel<true><<<(unsigned)grid, kPartThreads, kPartSmem, st>>>(pb_desc, pb_bin, n_seg, seg_b, chunk_b,
                                                                    kGroupShift, cur_b, packed, nullptr);
-  if (a.max_windows >= (1ull << 32))
+  // the 64-bit-counter instance is needed only when a fine bin could reach 2^32 windows;
+  // GERBIL_REGROUP_WIDE=1 forces it (tests)
+  const char* fw = getenv("GERBIL_REGROUP_WIDE");  // read per call (tests set it in-process)
+  const bool force_wide = fw && atoi(fw) == 1;
+  if (a.max_windows >= (1ull << 32) || force_wide)
     regroup_counted_kernel<true><<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);
   else
     regroup_counted_kernel<false><<<G, kFineT, 0, st>>>(packed, goff, a.n_bins, a.off, a.win, a.desc_out);

@@ -506,3 +506,22 @@ def test_device_sorted_fetch_matches_lexsort(G, k, read_len):
     order = np.lexsort(tuple(uk[:, j] for j in reversed(range(uk.shape[1]))))
     assert np.array_equal(sk, uk[order]) and np.array_equal(sc, uc[order])
     assert np.array_equal(sk2, sk) and np.array_equal(sc2, sc)
+
+
+@pytest.mark.parametrize("k,bins", [(40, 1 << 16), (28, 1 << 22)])
+def test_group_shuffle_wide_counters(G, monkeypatch, k, bins):
+    # the bin shuffle's 64-bit-counter regroup instance (needed only when a fine bin could hold
+    # 2^32 windows) forced on a small input: same histogram
+    import torch
+
+    monkeypatch.setenv("GERBIL_REGROUP_WIDE", "1")
+    text = synth.fastx(C0, synth.FASTQ)
+    ref = oracle.count(text, k, 1)
+    codes, nmask, rs = synth.packed_device(C0)
+    torch.cuda.synchronize()
+    with G.Gerbil(n_bins=bins) as g:
+        g.count_device(codes, nmask, rs, C0.n_reads, k, 15, 1)
+        keys, counts = g.fetch(sorted=True)
+        st = g.stats()
+    compare(keys, counts, k, ref)
+    assert st["count_sum"] == ref.windows
