@@ -2,6 +2,7 @@
 # Copy one r02b_final.sh evidence directory into profiles/ (benches, launch list, ncu summaries,
 # roofline_traffic.json):  bash scripts/r02_collect.sh gpurun_out
 set -eu
+shopt -s nullglob
 src=${1:-gpurun_out}
 for f in "$src"/r02_bench*.json; do cp "$f" profiles/; done
 [ -s "$src/r02_gpu_tests.txt" ] && { echo "# r02: python -m pytest tests -m gpu on one B200 (scripts/r02b_final.sh)"; tail -22 "$src/r02_gpu_tests.txt"; } > profiles/r02_gpu_tests.txt
