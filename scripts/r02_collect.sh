@@ -6,8 +6,10 @@ shopt -s nullglob
 src=${1:-gpurun_out}
 for f in "$src"/r02_bench*.json; do cp "$f" profiles/; done
 [ -s "$src/r02_gpu_tests.txt" ] && { echo "# r02: python -m pytest tests -m gpu on one B200 (scripts/r02b_final.sh)"; tail -22 "$src/r02_gpu_tests.txt"; } > profiles/r02_gpu_tests.txt
-{ echo "# r02 ncu launch list of one timed C1 step (bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline; ncu --metrics gpu__time_duration.sum --clock-control none: cold, serialised)";
-  python scripts/launch_summary.py "$src/r02_launches.csv"; } > profiles/r02_launches.txt
+if [ -s "$src/r02_launches.csv" ]; then
+  { echo "# r02 ncu launch list of one timed C1 step (bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline; ncu --metrics gpu__time_duration.sum --clock-control none: cold, serialised)";
+    python scripts/launch_summary.py "$src/r02_launches.csv"; } > profiles/r02_launches.txt
+fi
 python scripts/roofline_traffic.py "$src" profiles/r02 > /dev/null
 for d in "$src"/details_*.txt; do
   name=$(basename "$d" .txt); name=${name#details_}
