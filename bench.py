@@ -289,11 +289,19 @@ def roofline_report(st: dict, ms: float, per_kernel: dict, steps: int, P: int) -
     if kname in ("count_smem_kernel", "count_ref_kernel") and tr.get("warp_inst_per_step"):
         sms, clk = 148, tr.get("sm_mhz", 1965.0) * 1e6
         wi = float(tr["warp_inst_per_step"])
+        # the capture may hold fewer launches than a step (C4: the tier-1 launch only): then rate
+        # and per-window figures come from the captured launches alone (ncu's time, its windows
+        # approximated by the step's in proportion to time)
+        t_issue = kms
+        if int(tr.get("launches", launches)) < launches and tr.get("ms_per_step"):
+            t_issue = float(tr["ms_per_step"])
+        u_issue = units * min(1.0, t_issue / kms) if kms > 0 else units
         roof["issue"] = {
-            "bound": "issue", "unit": "warp-inst/s", "warp_inst_per_window": wi / max(units, 1.0),
-            "warp_inst_per_round_of_32": 32 * wi / max(units, 1.0),
-            "achieved": wi / (kms / 1e3) if kms > 0 else None, "peak": 4 * sms * clk,
-            "frac": (wi / (kms / 1e3)) / (4 * sms * clk) if kms > 0 else None,
+            "bound": "issue", "unit": "warp-inst/s", "warp_inst_per_window": wi / max(u_issue, 1.0),
+            "warp_inst_per_round_of_32": 32 * wi / max(u_issue, 1.0),
+            "achieved": wi / (t_issue / 1e3) if t_issue > 0 else None, "peak": 4 * sms * clk,
+            "frac": (wi / (t_issue / 1e3)) / (4 * sms * clk) if t_issue > 0 else None,
+            "captured_launches": int(tr.get("launches", launches)), "captured_ms": t_issue,
             "ipc_ncu": tr.get("ipc"), "issue_slots_busy_ncu": tr.get("issue_slots_busy"),
             "source": tr.get("source"),
             "note": "4 warp-instructions per cycle per SM x 148 SMs x SM clock (B200_PROFILING.md)"}
