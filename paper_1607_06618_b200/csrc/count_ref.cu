@@ -101,6 +101,9 @@ static_assert(kRB1 * kRI1 == 1u && kRB2 * kRI2 == 1u, "inverse multipliers");
 #ifndef GERBIL_REF_DEFER
 #define GERBIL_REF_DEFER 1
 #endif
+#ifndef GERBIL_REF_DEFER_SHORT
+#define GERBIL_REF_DEFER_SHORT 1  // the short-super-mer path defers its verifications too
+#endif
 #ifndef GERBIL_REF_ROLL
 #define GERBIL_REF_ROLL 2
 #endif
@@ -166,6 +169,21 @@ __device__ __noinline__ uint64_t direct_roll_hash(const uint64_t* codes, uint64_
     h2 = h2 * kRB2 + b;
   }
   return fmix64((uint64_t)h1 << 32 | h2);
+}
+
+// the short path's hash of the occurrence (q, rc): key_hash of its canonical k-mer (used when a
+// deferred verification finds another k-mer under the same fingerprint)
+template <int W>
+__device__ __noinline__ uint64_t direct_key_hash(const uint64_t* codes, uint64_t q, uint32_t k, bool rc) {
+  uint64_t c[W];
+  extract_kmer<W>(codes, q, k, c);
+  if (rc) {
+    uint64_t r[W];
+    reverse_complement<W>(c, k, r);
+#pragma unroll
+    for (int w = 0; w < W; ++w) c[w] = r[w];
+  }
+  return key_hash<W>(c);
 }
 
 template <int W>
@@ -235,6 +253,7 @@ __global__ void __launch_bounds__(NT, ref_ctas_per_sm<NT>()) count_ref_kernel(Sm
       s_ocur = 0;
     }
     __syncthreads();
+    const bool roll_bin = roll && avg >= (float)kLongSm;  // this bin's windows use the rolling hashes
     // one window per lane: probe / claim / verify (eqf compares the slot's k-mer with ours),
     // then (warp-wide) the occupied-slot list
     auto probe = [&](bool act, uint64_t q, uint64_t hv, bool rc, auto&& eqf) {
@@ -304,7 +323,7 @@ __global__ void __launch_bounds__(NT, ref_ctas_per_sm<NT>()) count_ref_kernel(Sm
           if (same_kmer<W>(a.codes, k, q, rc, (v >> 1) & kPosMask, (v & 1ull) != 0)) {
             atomicAdd(s_cnt + h, 1u);
           } else {
-            const uint64_t hv = direct_roll_hash(a.codes, q, k, rc);
+            const uint64_t hv = roll_bin ? direct_roll_hash(a.codes, q, k, rc) : direct_key_hash<W>(a.codes, q, k, rc);
             const uint64_t ref = kOcc | (((hv >> 41) & fpm) << kFpShift) | (q << 1) | (rc ? 1ull : 0ull);
             for (;;) {
               h = (h + 1 == cap) ? 0u : h + 1;
@@ -374,6 +393,18 @@ __global__ void __launch_bounds__(NT, ref_ctas_per_sm<NT>()) count_ref_kernel(Sm
       vq_n += __popc(dm);
       __syncwarp();
       if (vq_n >= 32) drain();
+    };
+    // short super-mers with the deferred verification: the canonical key is extracted and hashed
+    // whole; a fingerprint match is queued like on the rolling path
+    auto process_defer = [&](bool act, uint64_t q) {
+      bool rc = false;
+      uint64_t hv = 0;
+      if (act) {
+        uint64_t c[W];
+        rc = canon_at<W>(a.codes, q, k, canonical, c);
+        hv = key_hash<W>(c);
+      }
+      probe_defer(act, q, hv, rc);
     };
 #endif
     // long super-mers (k >= 32): n <= kPiece consecutive windows from q0, lanes = consecutive
@@ -493,12 +524,22 @@ __global__ void __launch_bounds__(NT, ref_ctas_per_sm<NT>()) count_ref_kernel(Sm
           if (!act) j = 0;
           const uint64_t pj = __shfl_sync(kFull, pos, j);
           const uint32_t ej = __shfl_sync(kFull, excl, j);
+#if GERBIL_REF_DEFER && GERBIL_REF_DEFER_SHORT
+          process_defer(act, pj + (i - ej));
+#else
           process(act, pj + (i - ej));
+#endif
         }
         uint32_t nu = 0;  // next unit: a dynamic counter per bin (units differ in length)
         if (lane == 0) nu = atomicAdd(&s_unit, 1u);
         u = __shfl_sync(kFull, nu, 0);
       }
+#if GERBIL_REF_DEFER && GERBIL_REF_DEFER_SHORT
+      if (vq_n) {
+        if (*(volatile int*)&s_abandon == 0) drain();  // the block-wide barrier below orders it
+        vq_n = 0;
+      }
+#endif
     } else {
       // long super-mers (long reads): a unit = one piece of <= 32 (k < 32) or kPiece (rolling
       // hashes) consecutive windows of one super-mer, numbered over the bin's descriptors (a block
